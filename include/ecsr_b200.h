@@ -1,0 +1,151 @@
+/*
+ * ecsr_b200.h -- C-ABI of libecsr_b200.so, the B200-native EC-CSR SpMV hot path.
+ *
+ * The reference's drop-in boundary for this path is the kernel-backend module
+ * protocol of `pkg/src/ecsr/_kernels.py:17-71`: a module exposing NAME,
+ * overlap_counts(...) and spmv_set(...), selected with use_backend(name).
+ * Its compiled implementation is `pkg/src/ecsr/_speedups.pyx:55-129`.
+ *
+ *   ecsr_b200_spmv_set   replaces _speedups.spmv_set          (_speedups.pyx:55-78)
+ *                        -- same arguments, host arrays, y accumulated in place,
+ *                        precision chosen by y's dtype, canonical arithmetic order
+ *                        (_speedups.pyx:81-129).
+ *   ecsr_b200_pack       replaces the per-call validate_container + set loop of
+ *                        executor.spmv_ec (executor.py:50-96): validates ONCE
+ *                        and uploads a device-resident, TMA-tiled layout.
+ *   ecsr_b200_spmv       replaces executor.spmv_ec(ec, x, validate=False)
+ *                        (executor.py:80-96) on device buffers, stream-ordered.
+ *   ecsr_b200_unpack     inverse of pack: reproduces the reference set arrays
+ *                        (storage.py:50-62) from device memory, for the
+ *                        bit-exact encoding check.
+ *   ecsr_b200_bytes      byte model of storage_report (storage.py:579-649) plus
+ *                        the device layout's actual bytes (roofline numerator).
+ *
+ * Return codes map onto ecsr.errors (errors.py:4-16) in the Python shim:
+ *   0 OK, 1 ContainerError, 2 ValueError (shape/dtype/argument), 3 CUDA error.
+ * Every failing call sets a thread-local message, read with ecsr_b200_last_error().
+ * No entry point synchronises the device except ecsr_b200_spmv_set and
+ * ecsr_b200_unpack (which return host data).
+ */
+#ifndef ECSR_B200_H
+#define ECSR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECSR_OK 0
+#define ECSR_ERR_CONTAINER 1
+#define ECSR_ERR_VALUE 2
+#define ECSR_ERR_CUDA 3
+
+/* element types (host values, device values, x and y) */
+#define ECSR_F16 1
+#define ECSR_F32 2
+#define ECSR_F64 3
+
+/* ecsr_b200_pack flags */
+#define ECSR_PACK_DEFAULT 0
+#define ECSR_PACK_FORCE_GENERIC 1 /* skip the tiled fast layout (parity/debug) */
+
+/* ecsr_b200_spmv modes */
+#define ECSR_SPMV_OVERWRITE 0   /* y  = A x */
+#define ECSR_SPMV_ACCUMULATE 1  /* y += A x */
+#define ECSR_SPMV_ORDERED 2     /* OR-flag: per-block partials + ordered per-row sum;
+                                   bitwise-reproducible, reference order
+                                   (executor.py:89 + _speedups.pyx:128-129) */
+
+/* One block set, exactly the arrays of ecsr.storage.EcCsrSet (storage.py:50-62). */
+typedef struct ecsr_host_set {
+    int32_t granularity;           /* g rows per block */
+    int32_t vector_size;           /* v columns per lane per warp step */
+    int64_t num_blocks;
+    int64_t stored_cols;           /* block_indptr[num_blocks] */
+    int64_t real_nnz;
+    const uint32_t* row_indices;   /* [g * num_blocks] */
+    const int64_t* block_indptr;   /* [num_blocks + 1] */
+    const uint32_t* base_indices;  /* [warp * num_blocks] */
+    const uint32_t* delta_indices; /* [stored_cols], chunk-permuted */
+    const uint8_t* pad_mask;       /* [stored_cols] bool bytes (cold: never read by kernels) */
+    const void* block_values;      /* [g * stored_cols], chunk-permuted, value_dtype */
+} ecsr_host_set;
+
+/* Output of ecsr_b200_unpack: caller-allocated arrays sized from ecsr_b200_set_info. */
+typedef struct ecsr_out_set {
+    uint32_t* row_indices;
+    int64_t* block_indptr;
+    uint32_t* base_indices;
+    uint32_t* delta_indices;
+    uint8_t* pad_mask;
+    void* block_values;            /* written in `out_value_dtype` */
+} ecsr_out_set;
+
+typedef struct ecsr_set_info {
+    int32_t granularity;
+    int32_t vector_size;
+    int64_t num_blocks;
+    int64_t stored_cols;
+    int64_t real_nnz;
+} ecsr_set_info;
+
+typedef struct ecsr_bytes {
+    /* storage_report(value_bits=16) components (storage.py:592-613) */
+    int64_t row_indices, block_indptr, base_indices, delta_indices, pad_mask, block_values, desc;
+    int64_t model_kernel_bytes; /* components - pad_mask - desc + 2K (x f16) + 4M (y f32) */
+    int64_t device_arena_bytes; /* bytes the fast kernel streams from HBM per SpMV */
+    int64_t device_total_bytes; /* every device allocation owned by the handle */
+    int32_t layout;             /* 1 = tiled fast layout, 2 = generic */
+    int32_t grid;               /* CTAs of the fast kernel */
+    int32_t stages;             /* smem ring depth */
+    int32_t stage_bytes;
+    int64_t tiles;
+} ecsr_bytes;
+
+typedef struct ecsr_dev ecsr_dev; /* opaque; immutable after pack */
+
+/* Validate + pack + upload. device_dtype: ECSR_F16 (the product: fp16 values and x,
+ * fp32 accumulate and y), ECSR_F32 or ECSR_F64 (generic kernel, container precision). */
+int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, int64_t num_cols,
+                   int32_t warp_size, int32_t delta_bits, int32_t value_bits,
+                   int32_t host_value_dtype, int32_t device_dtype, int32_t flags,
+                   ecsr_dev** out);
+
+/* y = A x (or y += A x). x: device [num_cols] of the handle's x type (f16 for an
+ * ECSR_F16 handle), y: device [num_rows] (f32 for ECSR_F16/F32, f64 for F64).
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream). */
+int ecsr_b200_spmv(const ecsr_dev* dev, const void* x, void* y, int32_t mode, void* stream);
+
+int ecsr_b200_info(const ecsr_dev* dev, int64_t* num_rows, int64_t* num_cols, int32_t* nsets,
+                   int32_t* warp_size, int32_t* delta_bits, int32_t* value_bits,
+                   int32_t* device_dtype);
+int ecsr_b200_set_info(const ecsr_dev* dev, int32_t set, ecsr_set_info* info);
+int ecsr_b200_unpack(const ecsr_dev* dev, ecsr_out_set* out, int32_t nsets,
+                     int32_t out_value_dtype);
+int ecsr_b200_bytes(const ecsr_dev* dev, ecsr_bytes* out);
+void ecsr_b200_free(ecsr_dev* dev);
+
+/* The reference backend protocol entry (_speedups.pyx:55-78): host arrays, one set,
+ * y (host, y_dtype ECSR_F32 or ECSR_F64) accumulated in place in the canonical
+ * order. values/x are given in y's precision (the shim coerces like
+ * np.ascontiguousarray(dtype=...) does). Synchronous. */
+int ecsr_b200_spmv_set(int32_t g, int32_t warp_size, int32_t vector_size, int64_t num_blocks,
+                       const uint32_t* row_ids, const int64_t* block_indptr,
+                       const uint32_t* base_indices, const uint32_t* delta_indices,
+                       const void* block_values, const void* x, int64_t x_len, void* y,
+                       int64_t y_len, int32_t y_dtype);
+
+/* IEEE round-to-nearest-even conversion used by pack (exposed for tests). */
+int ecsr_b200_to_f16(const void* src, int32_t src_dtype, uint16_t* dst, int64_t n);
+
+const char* ecsr_b200_last_error(void);
+const char* ecsr_b200_version(void);
+int ecsr_b200_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECSR_B200_H */

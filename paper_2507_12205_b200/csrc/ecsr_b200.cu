@@ -1,0 +1,888 @@
+// ecsr_b200.cu -- libecsr_b200.so: packer, launchers and the C-ABI of include/ecsr_b200.h.
+//
+// Host responsibilities:
+//   * validate a container once (executor.py:50-77, storage.py:312-329) instead of per call;
+//   * convert values to fp16 (IEEE RNE) and build the tiled, block-major device arena the
+//     fast kernel streams with bulk async copies; byte-balance tiles over a persistent grid;
+//   * build the slot tables of the ordered (bitwise-reproducible) y reduction;
+//   * keep the cold section (pad_mask, set descriptors) on the host for exact unpack;
+//   * expose the reference backend-protocol call spmv_set (_speedups.pyx:55-78).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ecsr_b200.h"
+#include "ecsr_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define ECSR_CUDA(expr)                                                                  \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(ECSR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int kTileTarget = 8192;       // bytes of whole blocks per tile (balance granularity)
+constexpr int kMaxStageBytes = 65536;   // largest tile a ring slot may hold
+constexpr int kMaxStages = 16;
+constexpr int kPackInternal = 1 << 30;  // spmv_set: unbounded u32 deltas (validated by range)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// IEEE-754 binary64 -> binary16, round to nearest even (also exact for f32 inputs).
+uint16_t f64_to_f16(double d) {
+    uint64_t bits;
+    std::memcpy(&bits, &d, 8);
+    const uint16_t sign = static_cast<uint16_t>((bits >> 48) & 0x8000u);
+    if (std::isnan(d)) return sign | 0x7e00u;
+    const double a = std::fabs(d);
+    if (a >= 65520.0) return sign | 0x7c00u;  // 65520 ties to even -> inf
+    if (a < 6.103515625e-05) {                 // below 2^-14: subnormal grid of 2^-24
+        const double q = std::nearbyint(a * 16777216.0);  // exact scaling, RNE
+        return sign | static_cast<uint16_t>(q);          // q == 1024 encodes 2^-14
+    }
+    int ex;
+    std::frexp(a, &ex);  // a = f * 2^ex, f in [0.5, 1)
+    int e = ex - 1;      // a in [2^e, 2^(e+1))
+    double m = std::nearbyint(std::ldexp(a, 10 - e));  // in [1024, 2048]
+    if (m >= 2048.0) {
+        m = 1024.0;
+        ++e;
+    }
+    if (e + 15 >= 31) return sign | 0x7c00u;
+    return sign | static_cast<uint16_t>(((e + 15) << 10) | (static_cast<int>(m) - 1024));
+}
+
+float f16_to_f32(uint16_t h) {
+    const uint32_t s = (h & 0x8000u) << 16;
+    const uint32_t e = (h >> 10) & 0x1fu;
+    const uint32_t m = h & 0x3ffu;
+    float out;
+    if (e == 0) {
+        out = std::ldexp(static_cast<float>(m), -24);
+        uint32_t b;
+        std::memcpy(&b, &out, 4);
+        b |= s;
+        std::memcpy(&out, &b, 4);
+        return out;
+    }
+    uint32_t b;
+    if (e == 31)
+        b = s | 0x7f800000u | (m << 13);
+    else
+        b = s | ((e + 112) << 23) | (m << 13);
+    std::memcpy(&out, &b, 4);
+    return out;
+}
+
+double host_value(const void* vals, int dtype, int64_t i) {
+    if (dtype == ECSR_F64) return static_cast<const double*>(vals)[i];
+    if (dtype == ECSR_F32) return static_cast<const float*>(vals)[i];
+    return f16_to_f32(static_cast<const uint16_t*>(vals)[i]);
+}
+
+int elem_size(int dtype) { return dtype == ECSR_F64 ? 8 : dtype == ECSR_F32 ? 4 : 2; }
+
+struct SetDesc {
+    int32_t g = 0, v = 0;
+    int64_t nb = 0, stored = 0, real = 0;
+    int64_t slot0 = 0;    // global slot of (block 0, row 0)
+    int64_t row_off = 0;  // offset into concatenated row_indices (== slot0)
+    int64_t base_off = 0, indptr_off = 0, col_off = 0, val_off = 0;
+};
+
+template <typename T>
+T* dalloc_copy(const std::vector<T>& h, int64_t* total, cudaError_t* err) {
+    T* d = nullptr;
+    const size_t bytes = std::max<size_t>(h.size() * sizeof(T), 16);
+    *err = cudaMalloc(&d, bytes);
+    if (*err != cudaSuccess) return nullptr;
+    *total += static_cast<int64_t>(bytes);
+    if (!h.empty()) *err = cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return d;
+}
+
+}  // namespace
+
+struct ecsr_dev {
+    int device = 0;
+    int64_t M = 0, K = 0;
+    int32_t W = 0, B = 0, vbits = 16, dtype = ECSR_F16, layout = 2;
+    std::vector<SetDesc> sets;
+    std::vector<uint8_t> pad_mask;  // cold section, concatenated per set
+    int64_t nslots = 0;
+    // tiled layout
+    uint8_t* d_arena = nullptr;
+    int64_t arena_bytes = 0;
+    uint32_t* d_tile_start16 = nullptr;
+    int64_t ntiles = 0;
+    uint32_t* d_cta_tile = nullptr;
+    int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
+    // ordered reduction
+    void* d_partials = nullptr;
+    uint32_t* d_row_ptr = nullptr;
+    uint32_t* d_row_slots = nullptr;
+    // generic layout
+    uint32_t* d_bases = nullptr;
+    int64_t* d_indptr = nullptr;
+    uint32_t* d_deltas = nullptr;
+    void* d_values = nullptr;
+    uint32_t* d_rows = nullptr;
+    ecsr_bytes bytes{};
+    std::vector<void*> allocs;
+
+    ~ecsr_dev() {
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+// Structural + range validation (executor.py:50-77; storage.py:312-329), plus row
+// ids < num_rows (the reference leaves that to unchecked C; a device write must not).
+// B == 32 is internal (spmv_set): the reference's in-RAM u32 deltas carry no bit bound.
+int validate(const ecsr_host_set* sets, int nsets, int64_t M, int64_t K, int W, int B) {
+    if (W < 1 || W > 32) return fail(ECSR_ERR_VALUE, "warp_size must be in [1, 32]");
+    if (B != 4 && B != 8 && B != 16 && B != 32)
+        return fail(ECSR_ERR_VALUE, "delta_bits must be 4, 8 or 16");
+    if (M < 0 || K < 0) return fail(ECSR_ERR_VALUE, "negative matrix shape");
+    const uint64_t limit = B == 32 ? (1ull << 32) : (1ull << B);
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        if (s.granularity < 1 || s.vector_size < 1)
+            return fail(ECSR_ERR_CONTAINER, "set granularity and vector size must be positive");
+        if (s.num_blocks < 0 || s.stored_cols < 0)
+            return fail(ECSR_ERR_CONTAINER, "negative set size");
+        const int64_t nb = s.num_blocks, g = s.granularity, v = s.vector_size;
+        if (nb > 0 && (!s.block_indptr || !s.row_indices || !s.base_indices))
+            return fail(ECSR_ERR_VALUE, "null set array");
+        if (s.stored_cols > 0 && (!s.delta_indices || !s.block_values))
+            return fail(ECSR_ERR_VALUE, "null set array");
+        if (nb == 0) {
+            if (s.stored_cols != 0)
+                return fail(ECSR_ERR_CONTAINER, "block_indptr does not cover stored columns");
+            continue;
+        }
+        if (s.block_indptr[0] != 0)
+            return fail(ECSR_ERR_CONTAINER, "block_indptr must start at 0 and be non-decreasing");
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t w = s.block_indptr[b + 1] - s.block_indptr[b];
+            if (w < 0)
+                return fail(ECSR_ERR_CONTAINER, "block_indptr must start at 0 and be non-decreasing");
+            if (w % (static_cast<int64_t>(W) * v))
+                return fail(ECSR_ERR_CONTAINER,
+                            "block widths must be multiples of warp_size * vector_size");
+        }
+        if (s.block_indptr[nb] != s.stored_cols)
+            return fail(ECSR_ERR_CONTAINER, "block_indptr does not cover stored columns");
+        for (int64_t i = 0; i < s.stored_cols; ++i)
+            if (s.delta_indices[i] >= limit)
+                return fail(ECSR_ERR_CONTAINER, "delta " + std::to_string(s.delta_indices[i]) +
+                                                    " exceeds " + std::to_string(B) + "-bit range");
+        for (int64_t i = 0; i < nb * W; ++i)
+            if (s.base_indices[i] >= static_cast<uint64_t>(std::max<int64_t>(K, 1)))
+                return fail(ECSR_ERR_CONTAINER, "base index out of range");
+        for (int64_t i = 0; i < nb * g; ++i)
+            if (s.row_indices[i] >= static_cast<uint64_t>(std::max<int64_t>(M, 1)))
+                return fail(ECSR_ERR_CONTAINER, "row index out of range");
+        std::vector<int64_t> top(W);
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t start = s.block_indptr[b], n = s.block_indptr[b + 1] - start;
+            if (n == 0) continue;
+            for (int t = 0; t < W; ++t) top[t] = s.base_indices[b * W + t];
+            const int64_t chunk = static_cast<int64_t>(W) * v;
+            for (int64_t i = 0; i < n; ++i) top[(i % chunk) / v] += s.delta_indices[start + i];
+            for (int t = 0; t < W; ++t)
+                if (top[t] >= K)
+                    return fail(ECSR_ERR_CONTAINER, "decoded column " + std::to_string(top[t]) +
+                                                        " out of range " + std::to_string(K));
+        }
+    }
+    return ECSR_OK;
+}
+
+bool pow2_le32(int g) { return g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32; }
+
+int tiled_header_bytes(int g) { return static_cast<int>(round_up(8 + 4 * g, 16)); }
+
+int64_t tiled_record_bytes(int g, int64_t n, bool wide) {
+    return tiled_header_bytes(g) + (wide ? 128 : 64) + n + 2 * g * n;
+}
+
+struct DeviceLimits {
+    int sms = 148;
+    int smem_optin = 232448;
+};
+
+int query_limits(int device, DeviceLimits* lim) {
+    ECSR_CUDA(cudaDeviceGetAttribute(&lim->sms, cudaDevAttrMultiProcessorCount, device));
+    ECSR_CUDA(cudaDeviceGetAttribute(&lim->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    return ECSR_OK;
+}
+
+// Build the block-major tiled arena (record layout: ecsr_kernels.cuh, tiled_block).
+void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<SetDesc>& desc,
+                       int host_dtype, bool wide, std::vector<uint8_t>* arena,
+                       std::vector<uint32_t>* tile_start16, int64_t* max_tile) {
+    arena->clear();
+    tile_start16->clear();
+    *max_tile = 0;
+    std::vector<std::pair<int, int64_t>> cur;  // (set, block) of the open tile
+    int64_t cur_bytes = 0;                     // record bytes of the open tile
+    auto hdr_of = [](size_t nblk) { return round_up(4 + 2 * static_cast<int64_t>(nblk), 16); };
+    auto flush = [&]() {
+        if (cur.empty()) return;
+        const int64_t start = static_cast<int64_t>(arena->size());
+        const int64_t hdr = hdr_of(cur.size());
+        arena->resize(start + hdr + cur_bytes, 0);
+        uint8_t* base = arena->data() + start;
+        const uint32_t nblk = static_cast<uint32_t>(cur.size());
+        std::memcpy(base, &nblk, 4);
+        int64_t off = hdr;
+        for (size_t i = 0; i < cur.size(); ++i) {
+            const ecsr_host_set& s = sets[cur[i].first];
+            const SetDesc& d = desc[cur[i].first];
+            const int64_t b = cur[i].second;
+            const int g = s.granularity, v = s.vector_size;
+            const int64_t st = s.block_indptr[b], n = s.block_indptr[b + 1] - st;
+            const uint16_t off16 = static_cast<uint16_t>(off / 16);
+            std::memcpy(base + 4 + 2 * i, &off16, 2);
+            uint8_t* r = base + off;
+            const uint32_t slot0 = static_cast<uint32_t>(d.slot0 + b * g);
+            const uint16_t nchunk = static_cast<uint16_t>(n / (32 * v));
+            std::memcpy(r, &slot0, 4);
+            std::memcpy(r + 4, &nchunk, 2);
+            r[6] = static_cast<uint8_t>(g);
+            r[7] = static_cast<uint8_t>(v);
+            std::memcpy(r + 8, s.row_indices + b * g, 4 * g);
+            uint8_t* q = r + tiled_header_bytes(g);
+            for (int t = 0; t < 32; ++t) {
+                const uint32_t bv = s.base_indices[b * 32 + t];
+                if (wide) {
+                    std::memcpy(q + 4 * t, &bv, 4);
+                } else {
+                    const uint16_t b16 = static_cast<uint16_t>(bv);
+                    std::memcpy(q + 2 * t, &b16, 2);
+                }
+            }
+            q += wide ? 128 : 64;
+            for (int64_t i2 = 0; i2 < n; ++i2) q[i2] = static_cast<uint8_t>(s.delta_indices[st + i2]);
+            q += n;
+            uint16_t* hv = reinterpret_cast<uint16_t*>(q);
+            for (int64_t i2 = 0; i2 < n * g; ++i2)
+                hv[i2] = f64_to_f16(host_value(s.block_values, host_dtype, st * g + i2));
+            off += tiled_record_bytes(g, n, wide);
+        }
+        tile_start16->push_back(static_cast<uint32_t>(start / 16));
+        *max_tile = std::max<int64_t>(*max_tile, hdr + cur_bytes);
+        cur.clear();
+        cur_bytes = 0;
+    };
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        for (int64_t b = 0; b < s.num_blocks; ++b) {
+            const int64_t n = s.block_indptr[b + 1] - s.block_indptr[b];
+            const int64_t rec = tiled_record_bytes(s.granularity, n, wide);
+            if (!cur.empty() && hdr_of(cur.size() + 1) + cur_bytes + rec > kTileTarget) flush();
+            cur.emplace_back(si, b);
+            cur_bytes += rec;
+        }
+    }
+    flush();
+    tile_start16->push_back(static_cast<uint32_t>(arena->size() / 16));
+}
+
+int build_slots(ecsr_dev* d, const ecsr_host_set* sets, int nsets, int64_t* total) {
+    std::vector<uint32_t> cnt(d->M + 1, 0);
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        for (int64_t b = 0; b < s.num_blocks; ++b) {
+            if (s.block_indptr[b + 1] == s.block_indptr[b]) continue;  // skipped by the kernel
+            for (int k = 0; k < s.granularity; ++k) cnt[s.row_indices[b * s.granularity + k] + 1]++;
+        }
+    }
+    std::vector<uint32_t> row_ptr(d->M + 1, 0);
+    for (int64_t r = 0; r < d->M; ++r) row_ptr[r + 1] = row_ptr[r] + cnt[r + 1];
+    std::vector<uint32_t> fill(row_ptr.begin(), row_ptr.begin() + d->M);
+    std::vector<uint32_t> slots(row_ptr[d->M]);
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        for (int64_t b = 0; b < s.num_blocks; ++b) {
+            if (s.block_indptr[b + 1] == s.block_indptr[b]) continue;
+            for (int k = 0; k < s.granularity; ++k) {
+                const uint32_t r = s.row_indices[b * s.granularity + k];
+                slots[fill[r]++] = static_cast<uint32_t>(d->sets[si].slot0 + b * s.granularity + k);
+            }
+        }
+    }
+    cudaError_t err = cudaSuccess;
+    d->d_row_ptr = dalloc_copy(row_ptr, total, &err);
+    if (d->d_row_ptr) d->allocs.push_back(d->d_row_ptr);
+    ECSR_CUDA(err);
+    d->d_row_slots = dalloc_copy(slots, total, &err);
+    if (d->d_row_slots) d->allocs.push_back(d->d_row_slots);
+    ECSR_CUDA(err);
+    const size_t pbytes = std::max<size_t>(16, d->nslots * (d->dtype == ECSR_F64 ? 8 : 4));
+    ECSR_CUDA(cudaMalloc(&d->d_partials, pbytes));
+    d->allocs.push_back(d->d_partials);
+    *total += static_cast<int64_t>(pbytes);
+    return ECSR_OK;
+}
+
+template <typename VT>
+void convert_values(const ecsr_host_set& s, int host_dtype, std::vector<VT>* out);
+template <>
+void convert_values<uint16_t>(const ecsr_host_set& s, int host_dtype, std::vector<uint16_t>* out) {
+    for (int64_t i = 0; i < s.stored_cols * s.granularity; ++i)
+        out->push_back(f64_to_f16(host_value(s.block_values, host_dtype, i)));
+}
+template <>
+void convert_values<float>(const ecsr_host_set& s, int host_dtype, std::vector<float>* out) {
+    for (int64_t i = 0; i < s.stored_cols * s.granularity; ++i)
+        out->push_back(static_cast<float>(host_value(s.block_values, host_dtype, i)));
+}
+template <>
+void convert_values<double>(const ecsr_host_set& s, int host_dtype, std::vector<double>* out) {
+    for (int64_t i = 0; i < s.stored_cols * s.granularity; ++i)
+        out->push_back(host_value(s.block_values, host_dtype, i));
+}
+
+template <typename VT>
+int build_generic(ecsr_dev* d, const ecsr_host_set* sets, int nsets, int host_dtype, int64_t* total) {
+    std::vector<uint32_t> bases, deltas, rows;
+    std::vector<int64_t> indptr;
+    std::vector<VT> vals;
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        SetDesc& sd = d->sets[si];
+        sd.base_off = static_cast<int64_t>(bases.size());
+        sd.indptr_off = static_cast<int64_t>(indptr.size());
+        sd.col_off = static_cast<int64_t>(deltas.size());
+        sd.val_off = static_cast<int64_t>(vals.size());
+        bases.insert(bases.end(), s.base_indices, s.base_indices + s.num_blocks * d->W);
+        if (s.num_blocks > 0) indptr.insert(indptr.end(), s.block_indptr, s.block_indptr + s.num_blocks + 1);
+        else indptr.push_back(0);
+        deltas.insert(deltas.end(), s.delta_indices, s.delta_indices + s.stored_cols);
+        rows.insert(rows.end(), s.row_indices, s.row_indices + s.num_blocks * s.granularity);
+        convert_values<VT>(s, host_dtype, &vals);
+    }
+    cudaError_t err = cudaSuccess;
+    d->d_bases = dalloc_copy(bases, total, &err);
+    if (d->d_bases) d->allocs.push_back(d->d_bases);
+    ECSR_CUDA(err);
+    d->d_indptr = dalloc_copy(indptr, total, &err);
+    if (d->d_indptr) d->allocs.push_back(d->d_indptr);
+    ECSR_CUDA(err);
+    d->d_deltas = dalloc_copy(deltas, total, &err);
+    if (d->d_deltas) d->allocs.push_back(d->d_deltas);
+    ECSR_CUDA(err);
+    d->d_rows = dalloc_copy(rows, total, &err);
+    if (d->d_rows) d->allocs.push_back(d->d_rows);
+    ECSR_CUDA(err);
+    VT* dv = dalloc_copy(vals, total, &err);
+    d->d_values = dv;
+    if (dv) d->allocs.push_back(dv);
+    ECSR_CUDA(err);
+    return ECSR_OK;
+}
+
+void fill_model_bytes(ecsr_dev* d, const ecsr_host_set* sets, int nsets) {
+    ecsr_bytes& b = d->bytes;
+    b.desc = 30 + 32 * static_cast<int64_t>(nsets);  // _HEADER_BYTES + _DESC_BYTES (storage.py:575-576)
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        b.row_indices += 4 * s.num_blocks * s.granularity;
+        b.block_indptr += 8 * (s.num_blocks + 1);
+        b.base_indices += 4 * s.num_blocks * d->W;
+        b.delta_indices += d->B == 4 ? (s.stored_cols + 1) / 2 : s.stored_cols * (d->B / 8);
+        b.pad_mask += (s.stored_cols + 7) / 8;
+        b.block_values += s.stored_cols * s.granularity * 16 / 8;
+    }
+    b.model_kernel_bytes = b.row_indices + b.block_indptr + b.base_indices + b.delta_indices +
+                           b.block_values + 2 * d->K + 4 * d->M;
+}
+
+int configure_tiled_kernels(int smem) {
+    static std::mutex mu;
+    static int configured = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (configured >= smem) return ECSR_OK;
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = smem;
+    return ECSR_OK;
+}
+
+template <typename K, typename... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <typename T, typename VT, typename XT>
+cudaError_t launch_generic_set(const ecsr_dev* d, const SetDesc& sd, const void* x, cudaStream_t st) {
+    ecsr::GenericSet gs;
+    gs.base_indices = d->d_bases + sd.base_off;
+    gs.block_indptr = d->d_indptr + sd.indptr_off;
+    gs.delta_indices = d->d_deltas + sd.col_off;
+    gs.block_values = static_cast<const VT*>(d->d_values) + sd.val_off;
+    gs.num_blocks = sd.nb;
+    gs.slot0 = sd.slot0;
+    gs.g = sd.g;
+    gs.warp = d->W;
+    gs.v = sd.v;
+    int p2 = 1;
+    while (p2 < d->W) p2 <<= 1;
+    gs.lanes_p2 = p2;
+    const int warps_per_cta = 8;
+    int64_t ctas = (sd.nb + warps_per_cta - 1) / warps_per_cta;
+    ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 16));
+    T* part = static_cast<T*>(d->d_partials);
+    const XT* xx = static_cast<const XT*>(x);
+    dim3 grid(static_cast<unsigned>(ctas)), block(32 * warps_per_cta);
+    if (sd.g <= 1) return launch_pdl(ecsr::ecsr_generic_kernel<T, VT, XT, 1>, grid, block, 0, st, gs, xx, part);
+    if (sd.g <= 2) return launch_pdl(ecsr::ecsr_generic_kernel<T, VT, XT, 2>, grid, block, 0, st, gs, xx, part);
+    if (sd.g <= 4) return launch_pdl(ecsr::ecsr_generic_kernel<T, VT, XT, 4>, grid, block, 0, st, gs, xx, part);
+    if (sd.g <= 8) return launch_pdl(ecsr::ecsr_generic_kernel<T, VT, XT, 8>, grid, block, 0, st, gs, xx, part);
+    return launch_pdl(ecsr::ecsr_generic_kernel<T, VT, XT, 16>, grid, block, 0, st, gs, xx, part);
+}
+
+template <typename T>
+cudaError_t launch_finish(const ecsr_dev* d, void* y, int accumulate, cudaStream_t st) {
+    const int threads = 256;
+    int64_t ctas = (d->M + threads - 1) / threads;
+    ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 8));
+    return launch_pdl(ecsr::ecsr_finish_rows<T>, dim3(static_cast<unsigned>(ctas)), dim3(threads), 0,
+                      st, static_cast<const uint32_t*>(d->d_row_ptr),
+                      static_cast<const uint32_t*>(d->d_row_slots),
+                      static_cast<const T*>(d->d_partials), static_cast<T*>(y), d->M, accumulate);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ecsr_b200_last_error(void) { return g_last_error.c_str(); }
+
+const char* ecsr_b200_version(void) { return "ecsr_b200 0.1.0 (sm_100a)"; }
+
+int ecsr_b200_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int ecsr_b200_to_f16(const void* src, int32_t src_dtype, uint16_t* dst, int64_t n) {
+    if (src_dtype != ECSR_F32 && src_dtype != ECSR_F64) return fail(ECSR_ERR_VALUE, "src dtype");
+    for (int64_t i = 0; i < n; ++i) dst[i] = f64_to_f16(host_value(src, src_dtype, i));
+    return ECSR_OK;
+}
+
+int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, int64_t num_cols,
+                   int32_t warp_size, int32_t delta_bits, int32_t value_bits,
+                   int32_t host_value_dtype, int32_t device_dtype, int32_t flags, ecsr_dev** out) {
+    if (!out) return fail(ECSR_ERR_VALUE, "out is null");
+    *out = nullptr;
+    if (nsets < 0 || (nsets > 0 && !sets)) return fail(ECSR_ERR_VALUE, "bad set list");
+    if (host_value_dtype != ECSR_F32 && host_value_dtype != ECSR_F64 && host_value_dtype != ECSR_F16)
+        return fail(ECSR_ERR_VALUE, "host values must be f16, f32 or f64");
+    if (device_dtype != ECSR_F16 && device_dtype != ECSR_F32 && device_dtype != ECSR_F64)
+        return fail(ECSR_ERR_VALUE, "device dtype must be f16, f32 or f64");
+    if (delta_bits == 32 && !(flags & kPackInternal)) return fail(ECSR_ERR_VALUE, "delta_bits must be 4, 8 or 16");
+    int rc = validate(sets, nsets, num_rows, num_cols, warp_size, delta_bits);
+    if (rc) return rc;
+
+    int64_t nslots = 0;
+    for (int si = 0; si < nsets; ++si) nslots += sets[si].num_blocks * sets[si].granularity;
+    if (nslots >= (1ll << 32) || num_rows >= (1ll << 32) - 1)
+        return fail(ECSR_ERR_VALUE, "container too large for 32-bit slot tables");
+
+    int dev = 0;
+    ECSR_CUDA(cudaGetDevice(&dev));
+    DeviceLimits lim;
+    rc = query_limits(dev, &lim);
+    if (rc) return rc;
+
+    auto* d = new ecsr_dev();
+    d->device = dev;
+    d->M = num_rows;
+    d->K = num_cols;
+    d->W = warp_size;
+    d->B = delta_bits;
+    d->vbits = value_bits;
+    d->dtype = device_dtype;
+    d->nslots = nslots;
+    d->sets.resize(nsets);
+    int64_t slot = 0;
+    for (int si = 0; si < nsets; ++si) {
+        SetDesc& sd = d->sets[si];
+        sd.g = sets[si].granularity;
+        sd.v = sets[si].vector_size;
+        sd.nb = sets[si].num_blocks;
+        sd.stored = sets[si].stored_cols;
+        sd.real = sets[si].real_nnz;
+        sd.slot0 = slot;
+        sd.row_off = slot;
+        slot += sd.nb * sd.g;
+        if (sets[si].pad_mask)
+            d->pad_mask.insert(d->pad_mask.end(), sets[si].pad_mask, sets[si].pad_mask + sd.stored);
+        else
+            d->pad_mask.insert(d->pad_mask.end(), sd.stored, 0);
+    }
+    fill_model_bytes(d, sets, nsets);
+    int64_t total = 0;
+
+    // Tiled fast layout: fp16 values, W = 32, deltas <= 8 bits, supported (g, v), x fits smem.
+    bool tiled = device_dtype == ECSR_F16 && !(flags & ECSR_PACK_FORCE_GENERIC) && warp_size == 32 &&
+                 delta_bits <= 8;
+    for (int si = 0; si < nsets && tiled; ++si) {
+        const int g = sets[si].granularity, v = sets[si].vector_size;
+        if (!pow2_le32(g) || !(v == 1 || v == 2 || v == 4 || v == 8)) tiled = false;
+        for (int64_t b = 0; b < sets[si].num_blocks && tiled; ++b)
+            if ((sets[si].block_indptr[b + 1] - sets[si].block_indptr[b]) / (32 * v) > 65535) tiled = false;
+    }
+    const bool wide = num_cols > 65535;
+    if (tiled) {
+        std::vector<uint8_t> arena;
+        std::vector<uint32_t> tstart;
+        int64_t max_tile = 0;
+        build_tiled_arena(sets, nsets, d->sets, host_value_dtype, wide, &arena, &tstart, &max_tile);
+        const int64_t stage = round_up(std::max<int64_t>(max_tile, kTileTarget), 128);
+        const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
+        const int64_t avail = lim.smem_optin - 1024 - 16 * kMaxStages - xbytes;
+        const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
+        if (stage > kMaxStageBytes || nst < 2 || arena.size() / 16 >= (1ull << 32)) tiled = false;
+        if (tiled) {
+            d->layout = 1;
+            d->wide = wide;
+            d->stage_bytes = static_cast<int>(stage);
+            d->nstages = static_cast<int>(nst);
+            d->smem_bytes = static_cast<int>(round_up(16 * nst, 128) + nst * stage + xbytes);
+            const int64_t ntiles = static_cast<int64_t>(tstart.size()) - 1;
+            d->ntiles = ntiles;
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(lim.sms, ntiles)));
+            d->grid = grid;
+            // byte-balanced contiguous tile ranges
+            std::vector<uint32_t> cta(grid + 1, 0);
+            const double total_bytes = static_cast<double>(arena.size());
+            int c = 1;
+            for (int64_t t = 0; t < ntiles && c < grid; ++t) {
+                const double mid = 16.0 * (0.5 * (static_cast<double>(tstart[t]) + tstart[t + 1]));
+                while (c < grid && mid >= total_bytes * c / grid) cta[c++] = static_cast<uint32_t>(t);
+            }
+            while (c < grid) cta[c++] = static_cast<uint32_t>(ntiles);
+            cta[grid] = static_cast<uint32_t>(ntiles);
+            for (int i = 1; i <= grid; ++i) cta[i] = std::max(cta[i], cta[i - 1]);
+            cudaError_t err = cudaSuccess;
+            d->arena_bytes = static_cast<int64_t>(arena.size());
+            d->d_arena = dalloc_copy(arena, &total, &err);
+            if (d->d_arena) d->allocs.push_back(d->d_arena);
+            if (err == cudaSuccess) {
+                d->d_tile_start16 = dalloc_copy(tstart, &total, &err);
+                if (d->d_tile_start16) d->allocs.push_back(d->d_tile_start16);
+            }
+            if (err == cudaSuccess) {
+                d->d_cta_tile = dalloc_copy(cta, &total, &err);
+                if (d->d_cta_tile) d->allocs.push_back(d->d_cta_tile);
+            }
+            if (err != cudaSuccess) {
+                delete d;
+                return fail(ECSR_ERR_CUDA, std::string("tiled upload: ") + cudaGetErrorString(err));
+            }
+            rc = configure_tiled_kernels(d->smem_bytes);
+            if (rc) {
+                delete d;
+                return rc;
+            }
+        }
+    }
+    if (!tiled) {
+        d->layout = 2;
+        if (device_dtype == ECSR_F16) rc = build_generic<uint16_t>(d, sets, nsets, host_value_dtype, &total);
+        else if (device_dtype == ECSR_F32) rc = build_generic<float>(d, sets, nsets, host_value_dtype, &total);
+        else rc = build_generic<double>(d, sets, nsets, host_value_dtype, &total);
+        if (rc) {
+            delete d;
+            return rc;
+        }
+    }
+    rc = build_slots(d, sets, nsets, &total);
+    if (rc) {
+        delete d;
+        return rc;
+    }
+    d->bytes.device_arena_bytes = d->layout == 1 ? d->arena_bytes : total;
+    d->bytes.device_total_bytes = total;
+    d->bytes.layout = d->layout;
+    d->bytes.grid = d->grid;
+    d->bytes.stages = d->nstages;
+    d->bytes.stage_bytes = d->stage_bytes;
+    d->bytes.tiles = d->ntiles;
+    *out = d;
+    return ECSR_OK;
+}
+
+int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void* stream) {
+    if (!d) return fail(ECSR_ERR_VALUE, "null handle");
+    if ((!x && d->K > 0) || (!y && d->M > 0)) return fail(ECSR_ERR_VALUE, "null x or y");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int accumulate = mode & ECSR_SPMV_ACCUMULATE;
+    const bool ordered = (mode & ECSR_SPMV_ORDERED) != 0 || d->layout == 2;
+    const size_t ysize = d->dtype == ECSR_F64 ? 8 : 4;
+    if (d->M == 0) return ECSR_OK;
+    if (d->layout == 1) {
+        if (!ordered && !accumulate) ECSR_CUDA(cudaMemsetAsync(y, 0, d->M * ysize, st));
+        ecsr::TiledParams p;
+        p.arena = d->d_arena;
+        p.tile_start16 = d->d_tile_start16;
+        p.cta_tile = d->d_cta_tile;
+        p.x = static_cast<const __half*>(x);
+        p.y = static_cast<float*>(y);
+        p.partials = static_cast<float*>(d->d_partials);
+        p.K = static_cast<int32_t>(d->K);
+        p.ordered = ordered ? 1 : 0;
+        p.stage_bytes = d->stage_bytes;
+        p.nstages = d->nstages;
+        p.x_vec16 = (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+        cudaError_t e;
+        if (d->wide)
+            e = launch_pdl(ecsr::ecsr_tiled_kernel<true>, dim3(d->grid), dim3(ecsr::kThreadsTiled),
+                           d->smem_bytes, st, p);
+        else
+            e = launch_pdl(ecsr::ecsr_tiled_kernel<false>, dim3(d->grid), dim3(ecsr::kThreadsTiled),
+                           d->smem_bytes, st, p);
+        ECSR_CUDA(e);
+        if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
+        return ECSR_OK;
+    }
+    for (const SetDesc& sd : d->sets) {
+        if (sd.nb == 0) continue;
+        cudaError_t e;
+        if (d->dtype == ECSR_F16) e = launch_generic_set<float, __half, __half>(d, sd, x, st);
+        else if (d->dtype == ECSR_F32) e = launch_generic_set<float, float, float>(d, sd, x, st);
+        else e = launch_generic_set<double, double, double>(d, sd, x, st);
+        ECSR_CUDA(e);
+    }
+    if (d->dtype == ECSR_F64) ECSR_CUDA(launch_finish<double>(d, y, accumulate, st));
+    else ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
+    return ECSR_OK;
+}
+
+int ecsr_b200_info(const ecsr_dev* d, int64_t* num_rows, int64_t* num_cols, int32_t* nsets,
+                   int32_t* warp_size, int32_t* delta_bits, int32_t* value_bits, int32_t* device_dtype) {
+    if (!d) return fail(ECSR_ERR_VALUE, "null handle");
+    if (num_rows) *num_rows = d->M;
+    if (num_cols) *num_cols = d->K;
+    if (nsets) *nsets = static_cast<int32_t>(d->sets.size());
+    if (warp_size) *warp_size = d->W;
+    if (delta_bits) *delta_bits = d->B;
+    if (value_bits) *value_bits = d->vbits;
+    if (device_dtype) *device_dtype = d->dtype;
+    return ECSR_OK;
+}
+
+int ecsr_b200_set_info(const ecsr_dev* d, int32_t set, ecsr_set_info* info) {
+    if (!d || !info) return fail(ECSR_ERR_VALUE, "null argument");
+    if (set < 0 || set >= static_cast<int32_t>(d->sets.size())) return fail(ECSR_ERR_VALUE, "set index");
+    const SetDesc& s = d->sets[set];
+    info->granularity = s.g;
+    info->vector_size = s.v;
+    info->num_blocks = s.nb;
+    info->stored_cols = s.stored;
+    info->real_nnz = s.real;
+    return ECSR_OK;
+}
+
+static void store_value(void* dst, int dtype, int64_t i, double v) {
+    if (dtype == ECSR_F64) static_cast<double*>(dst)[i] = v;
+    else if (dtype == ECSR_F32) static_cast<float*>(dst)[i] = static_cast<float>(v);
+    else static_cast<uint16_t*>(dst)[i] = f64_to_f16(v);
+}
+
+int ecsr_b200_unpack(const ecsr_dev* d, ecsr_out_set* out, int32_t nsets, int32_t out_value_dtype) {
+    if (!d || (!out && nsets > 0)) return fail(ECSR_ERR_VALUE, "null argument");
+    if (nsets != static_cast<int32_t>(d->sets.size())) return fail(ECSR_ERR_VALUE, "set count mismatch");
+    if (out_value_dtype != ECSR_F16 && out_value_dtype != ECSR_F32 && out_value_dtype != ECSR_F64)
+        return fail(ECSR_ERR_VALUE, "bad output dtype");
+    // cold section: pad_mask
+    int64_t moff = 0;
+    for (int si = 0; si < nsets; ++si) {
+        std::memcpy(out[si].pad_mask, d->pad_mask.data() + moff, d->sets[si].stored);
+        moff += d->sets[si].stored;
+    }
+    if (d->layout == 1) {
+        std::vector<uint8_t> arena(d->arena_bytes);
+        std::vector<uint32_t> tstart(d->ntiles + 1);
+        ECSR_CUDA(cudaMemcpy(arena.data(), d->d_arena, d->arena_bytes, cudaMemcpyDeviceToHost));
+        ECSR_CUDA(cudaMemcpy(tstart.data(), d->d_tile_start16, 4 * (d->ntiles + 1), cudaMemcpyDeviceToHost));
+        int si = 0;
+        int64_t b = 0;
+        while (si < nsets && d->sets[si].nb == 0) {
+            out[si].block_indptr[0] = 0;
+            ++si;
+        }
+        for (int64_t t = 0; t < d->ntiles; ++t) {
+            const uint8_t* tile = arena.data() + 16ull * tstart[t];
+            uint32_t nblk;
+            std::memcpy(&nblk, tile, 4);
+            for (uint32_t j = 0; j < nblk; ++j) {
+                if (si >= nsets) return fail(ECSR_ERR_CONTAINER, "arena holds more blocks than sets");
+                const SetDesc& sd = d->sets[si];
+                ecsr_out_set& o = out[si];
+                uint16_t off16;
+                std::memcpy(&off16, tile + 4 + 2 * j, 2);
+                const uint8_t* r = tile + 16 * off16;
+                uint16_t nchunk;
+                std::memcpy(&nchunk, r + 4, 2);
+                const int g = r[6], v = r[7];
+                if (g != sd.g || v != sd.v) return fail(ECSR_ERR_CONTAINER, "arena/set descriptor mismatch");
+                const int64_t n = static_cast<int64_t>(nchunk) * 32 * v;
+                if (b == 0) o.block_indptr[0] = 0;
+                o.block_indptr[b + 1] = o.block_indptr[b] + n;
+                std::memcpy(o.row_indices + b * g, r + 8, 4 * g);
+                const uint8_t* q = r + tiled_header_bytes(g);
+                for (int l = 0; l < 32; ++l) {
+                    if (d->wide) {
+                        std::memcpy(o.base_indices + b * 32 + l, q + 4 * l, 4);
+                    } else {
+                        uint16_t b16;
+                        std::memcpy(&b16, q + 2 * l, 2);
+                        o.base_indices[b * 32 + l] = b16;
+                    }
+                }
+                q += d->wide ? 128 : 64;
+                const int64_t st0 = o.block_indptr[b];
+                for (int64_t i = 0; i < n; ++i) o.delta_indices[st0 + i] = q[i];
+                q += n;
+                for (int64_t i = 0; i < n * g; ++i) {
+                    uint16_t h;
+                    std::memcpy(&h, q + 2 * i, 2);
+                    if (out_value_dtype == ECSR_F16) static_cast<uint16_t*>(o.block_values)[st0 * g + i] = h;
+                    else store_value(o.block_values, out_value_dtype, st0 * g + i, f16_to_f32(h));
+                }
+                if (++b == sd.nb) {
+                    b = 0;
+                    ++si;
+                    while (si < nsets && d->sets[si].nb == 0) {
+                        out[si].block_indptr[0] = 0;
+                        ++si;
+                    }
+                }
+            }
+        }
+        if (si != nsets) return fail(ECSR_ERR_CONTAINER, "arena holds fewer blocks than sets");
+        return ECSR_OK;
+    }
+    // generic layout: copy the reference arrays back
+    int64_t voff = 0;
+    const int esz = elem_size(d->dtype);
+    for (int si = 0; si < nsets; ++si) {
+        const SetDesc& sd = d->sets[si];
+        ecsr_out_set& o = out[si];
+        ECSR_CUDA(cudaMemcpy(o.block_indptr, d->d_indptr + sd.indptr_off, 8 * (sd.nb + 1), cudaMemcpyDeviceToHost));
+        if (sd.nb) {
+            ECSR_CUDA(cudaMemcpy(o.base_indices, d->d_bases + sd.base_off, 4 * sd.nb * d->W, cudaMemcpyDeviceToHost));
+            ECSR_CUDA(cudaMemcpy(o.row_indices, d->d_rows + sd.row_off, 4 * sd.nb * sd.g, cudaMemcpyDeviceToHost));
+        }
+        if (sd.stored) {
+            ECSR_CUDA(cudaMemcpy(o.delta_indices, d->d_deltas + sd.col_off, 4 * sd.stored, cudaMemcpyDeviceToHost));
+            std::vector<uint8_t> raw(sd.stored * sd.g * esz);
+            ECSR_CUDA(cudaMemcpy(raw.data(), static_cast<const uint8_t*>(d->d_values) + voff * esz, raw.size(),
+                                 cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < sd.stored * sd.g; ++i) {
+                if (out_value_dtype == d->dtype) {
+                    std::memcpy(static_cast<uint8_t*>(o.block_values) + i * esz, raw.data() + i * esz, esz);
+                } else {
+                    store_value(o.block_values, out_value_dtype, i, host_value(raw.data(), d->dtype, i));
+                }
+            }
+        }
+        voff += sd.stored * sd.g;
+    }
+    return ECSR_OK;
+}
+
+int ecsr_b200_bytes(const ecsr_dev* d, ecsr_bytes* out) {
+    if (!d || !out) return fail(ECSR_ERR_VALUE, "null argument");
+    *out = d->bytes;
+    return ECSR_OK;
+}
+
+void ecsr_b200_free(ecsr_dev* d) { delete d; }
+
+int ecsr_b200_spmv_set(int32_t g, int32_t warp_size, int32_t vector_size, int64_t num_blocks,
+                       const uint32_t* row_ids, const int64_t* block_indptr,
+                       const uint32_t* base_indices, const uint32_t* delta_indices,
+                       const void* block_values, const void* x, int64_t x_len, void* y,
+                       int64_t y_len, int32_t y_dtype) {
+    if (y_dtype != ECSR_F32 && y_dtype != ECSR_F64) return fail(ECSR_ERR_VALUE, "y must be f32 or f64");
+    if (num_blocks < 0) return fail(ECSR_ERR_VALUE, "negative block count");
+    ecsr_host_set s{};
+    s.granularity = g;
+    s.vector_size = vector_size;
+    s.num_blocks = num_blocks;
+    s.stored_cols = num_blocks > 0 ? block_indptr[num_blocks] : 0;
+    s.real_nnz = 0;
+    s.row_indices = row_ids;
+    s.block_indptr = block_indptr;
+    s.base_indices = base_indices;
+    s.delta_indices = delta_indices;
+    s.pad_mask = nullptr;
+    s.block_values = block_values;
+    // The reference kernel takes deltas as u32 and never range-checks them; accept any
+    // width up to 16 bits here and let validate() bound every decoded column.
+    ecsr_dev* d = nullptr;
+    int rc = ecsr_b200_pack(&s, 1, y_len, x_len, warp_size, 32, 16, y_dtype, y_dtype,
+                            ECSR_PACK_FORCE_GENERIC | kPackInternal, &d);
+    if (rc) return rc;
+    const size_t esz = y_dtype == ECSR_F64 ? 8 : 4;
+    void* dx = nullptr;
+    void* dy = nullptr;
+    int out = ECSR_OK;
+    cudaError_t e = cudaMalloc(&dx, std::max<size_t>(16, x_len * esz));
+    if (e == cudaSuccess) e = cudaMalloc(&dy, std::max<size_t>(16, y_len * esz));
+    if (e == cudaSuccess && x_len) e = cudaMemcpy(dx, x, x_len * esz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && y_len) e = cudaMemcpy(dy, y, y_len * esz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        out = ecsr_b200_spmv(d, dx, dy, ECSR_SPMV_ACCUMULATE | ECSR_SPMV_ORDERED, nullptr);
+        if (out == ECSR_OK) e = cudaDeviceSynchronize();
+        if (out == ECSR_OK && e == cudaSuccess && y_len) e = cudaMemcpy(y, dy, y_len * esz, cudaMemcpyDeviceToHost);
+    }
+    if (dx) cudaFree(dx);
+    if (dy) cudaFree(dy);
+    ecsr_b200_free(d);
+    if (out) return out;
+    if (e != cudaSuccess) return fail(ECSR_ERR_CUDA, std::string("spmv_set: ") + cudaGetErrorString(e));
+    return ECSR_OK;
+}
+
+}  // extern "C"

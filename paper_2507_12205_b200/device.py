@@ -1,0 +1,226 @@
+"""Device-resident EC-CSR matrices and the SpMV call (torch-facing API).
+
+`to_device(ec)` validates and packs a container once (`ecsr_b200_pack`); `spmv(W, x)`
+is the reference's `executor.spmv_ec(ec, x)` (`pkg/src/ecsr/executor.py:80-96`) on
+device tensors: x fp16 [K] -> y fp32 [M], stream-ordered, no host sync. PyTorch only
+supplies device memory and streams; all compute is in libecsr_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .container import EcCsrMatrix, EcCsrSet
+
+_DEVICE_DTYPES = {"f16": _lib.F16, "f32": _lib.F32, "f64": _lib.F64}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _host_sets(ec):
+    """Coerce a container's sets to the C-ABI dtypes (copies only on mismatch, like
+    np.ascontiguousarray in `_speedups.pyx:62-77`). Returns (HostSet array, keepalive)."""
+    dtype = np.dtype(ec.dtype)
+    if dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
+        raise ValueError("container values must be float32 or float64")
+    keep = []
+    arr = (_lib.HostSet * max(len(ec.sets), 1))()
+    for i, s in enumerate(ec.sets):
+        rows = np.ascontiguousarray(s.row_indices, dtype=np.uint32)
+        indptr = np.ascontiguousarray(s.block_indptr, dtype=np.int64)
+        bases = np.ascontiguousarray(s.base_indices, dtype=np.uint32)
+        deltas = np.ascontiguousarray(s.delta_indices, dtype=np.uint32)
+        mask = np.ascontiguousarray(s.pad_mask, dtype=np.bool_).view(np.uint8)
+        vals = np.ascontiguousarray(s.block_values, dtype=dtype)
+        keep += [rows, indptr, bases, deltas, mask, vals]
+        arr[i] = _lib.HostSet(int(s.granularity), int(s.vector_size), int(s.num_blocks),
+                              int(s.stored_cols), int(s.real_nnz), _lib.ptr(rows),
+                              _lib.ptr(indptr), _lib.ptr(bases), _lib.ptr(deltas),
+                              _lib.ptr(mask), _lib.ptr(vals))
+    return arr, keep, dtype
+
+
+class DeviceMatrix:
+    """Opaque handle to a packed container (immutable after pack)."""
+
+    def __init__(self, handle: int, num_rows: int, num_cols: int, device_dtype: str,
+                 device_index: int):
+        self._handle = ctypes.c_void_p(handle)
+        self.num_rows = num_rows
+        self.num_cols = num_cols
+        self.device_dtype = device_dtype
+        self.device_index = device_index
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if not self._handle:
+            raise ValueError("DeviceMatrix was freed")
+        return self._handle
+
+    def free(self) -> None:
+        if self._handle:
+            _lib.lib().ecsr_b200_free(self._handle)
+            self._handle = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # interpreter shutdown
+            pass
+
+    @property
+    def x_dtype(self):
+        torch = _torch()
+        return {"f16": torch.float16, "f32": torch.float32, "f64": torch.float64}[self.device_dtype]
+
+    @property
+    def y_dtype(self):
+        torch = _torch()
+        return torch.float64 if self.device_dtype == "f64" else torch.float32
+
+    def bytes(self) -> dict:
+        out = _lib.Bytes()
+        _lib.check(_lib.lib().ecsr_b200_bytes(self.handle, ctypes.byref(out)), "ecsr_b200_bytes")
+        return out.to_dict()
+
+    @property
+    def layout(self) -> str:
+        return {1: "tiled", 2: "generic"}[self.bytes()["layout"]]
+
+    def spmv(self, x, y=None, accumulate: bool = False, ordered: bool = False, stream=None):
+        return spmv(self, x, y=y, accumulate=accumulate, ordered=ordered, stream=stream)
+
+    def unpack(self, value_dtype=np.float32) -> EcCsrMatrix:
+        return unpack(self, value_dtype)
+
+
+def to_device(ec, device_dtype: str = "f16", force_generic: bool = False,
+              device=None) -> DeviceMatrix:
+    """Validate once and upload (replaces the per-call `validate_container`,
+    `executor.py:85-86`). Raises ContainerError exactly where the reference would."""
+    torch = _torch()
+    if device_dtype not in _DEVICE_DTYPES:
+        raise ValueError(f"device_dtype must be one of {sorted(_DEVICE_DTYPES)}")
+    dev = torch.device("cuda" if device is None else device)
+    index = dev.index if dev.index is not None else torch.cuda.current_device()
+    arr, keep, dtype = _host_sets(ec)
+    out = ctypes.c_void_p()
+    flags = _lib.PACK_FORCE_GENERIC if force_generic else _lib.PACK_DEFAULT
+    with torch.cuda.device(index):
+        rc = _lib.lib().ecsr_b200_pack(arr, len(ec.sets), int(ec.num_rows), int(ec.num_cols),
+                                       int(ec.warp_size), int(ec.delta_bits), int(ec.value_bits),
+                                       _lib.dtype_code(dtype), _DEVICE_DTYPES[device_dtype],
+                                       flags, ctypes.byref(out))
+    _lib.check(rc, "ecsr_b200_pack")
+    del keep
+    return DeviceMatrix(out.value, int(ec.num_rows), int(ec.num_cols), device_dtype, index)
+
+
+def spmv(W: DeviceMatrix, x, y=None, accumulate: bool = False, ordered: bool = False,
+         stream=None):
+    """y = W x (y += W x with accumulate). x: device tensor [K] of W.x_dtype.
+
+    ordered=True selects the bitwise-reproducible reduction (per-block partials summed
+    per row in container order, exactly the reference's y order); the default uses
+    red.global.add.f32 and is the fast path.
+    """
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError("x must be a CUDA tensor (use spmv_host for host buffers)")
+    if x.shape != (W.num_cols,):
+        raise ValueError(f"x has shape {tuple(x.shape)}, expected ({W.num_cols},)")
+    if x.dtype != W.x_dtype:
+        raise ValueError(f"x must be {W.x_dtype}, got {x.dtype}")
+    x = x.contiguous()
+    if y is None:
+        y = torch.empty(W.num_rows, dtype=W.y_dtype, device=x.device)
+        if accumulate:
+            y.zero_()
+    elif y.shape != (W.num_rows,) or y.dtype != W.y_dtype or not y.is_contiguous():
+        raise ValueError("y must be a contiguous device tensor of shape (num_rows,) and y dtype")
+    mode = (_lib.SPMV_ACCUMULATE if accumulate else _lib.SPMV_OVERWRITE) | (
+        _lib.SPMV_ORDERED if ordered else 0)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    rc = _lib.lib().ecsr_b200_spmv(W.handle, ctypes.c_void_p(x.data_ptr()),
+                                   ctypes.c_void_p(y.data_ptr()), mode,
+                                   ctypes.c_void_p(s.cuda_stream))
+    _lib.check(rc, "ecsr_b200_spmv")
+    return y
+
+
+def spmv_host(W: DeviceMatrix, x: np.ndarray, ordered: bool = False) -> np.ndarray:
+    """End-to-end call with host buffers: H2D x, SpMV, D2H y (synchronous)."""
+    torch = _torch()
+    xt = torch.from_numpy(np.ascontiguousarray(x).astype(
+        {"f16": np.float16, "f32": np.float32, "f64": np.float64}[W.device_dtype]))
+    xd = xt.to(f"cuda:{W.device_index}", non_blocking=False)
+    y = spmv(W, xd, ordered=ordered)
+    return y.cpu().numpy()
+
+
+def unpack(W: DeviceMatrix, value_dtype=np.float32) -> EcCsrMatrix:
+    """Read the device layout back into reference set arrays (`storage.py:50-62`)."""
+    lib = _lib.lib()
+    M, K = ctypes.c_int64(), ctypes.c_int64()
+    nsets, warp, dbits, vbits, ddt = (ctypes.c_int32() for _ in range(5))
+    _lib.check(lib.ecsr_b200_info(W.handle, ctypes.byref(M), ctypes.byref(K), ctypes.byref(nsets),
+                                  ctypes.byref(warp), ctypes.byref(dbits), ctypes.byref(vbits),
+                                  ctypes.byref(ddt)), "ecsr_b200_info")
+    vdt = np.dtype(value_dtype)
+    sets, outs = [], (_lib.OutSet * max(nsets.value, 1))()
+    for i in range(nsets.value):
+        info = _lib.SetInfo()
+        _lib.check(lib.ecsr_b200_set_info(W.handle, i, ctypes.byref(info)), "ecsr_b200_set_info")
+        g, nb, st = info.granularity, info.num_blocks, info.stored_cols
+        s = EcCsrSet(info.granularity, info.vector_size, nb, st, info.real_nnz,
+                     np.zeros(g * nb, np.uint32), np.zeros(nb + 1, np.int64),
+                     np.zeros(warp.value * nb, np.uint32), np.zeros(st, np.uint32),
+                     np.zeros(st, np.bool_), np.zeros(g * st, vdt))
+        sets.append(s)
+        outs[i] = _lib.OutSet(_lib.ptr(s.row_indices), s.block_indptr.ctypes.data,
+                              _lib.ptr(s.base_indices), _lib.ptr(s.delta_indices),
+                              _lib.ptr(s.pad_mask.view(np.uint8)), _lib.ptr(s.block_values))
+    _lib.check(lib.ecsr_b200_unpack(W.handle, outs, nsets.value, _lib.dtype_code(vdt)),
+               "ecsr_b200_unpack")
+    return EcCsrMatrix(M.value, K.value, vbits.value, dbits.value, warp.value, sets)
+
+
+def vstack(ecs) -> EcCsrMatrix:
+    """Stack containers by rows into one (fused QKV / gate-up): y = [A_0 x; A_1 x; ...].
+
+    The sets are concatenated in order with row ids offset, which is a valid
+    container for spmv_ec semantics (any set order is; executor.py:90-95).
+    """
+    ecs = list(ecs)
+    if not ecs:
+        raise ValueError("nothing to stack")
+    k = ecs[0].num_cols
+    w, b = ecs[0].warp_size, ecs[0].delta_bits
+    sets, off = [], 0
+    dtype = np.result_type(*[np.dtype(e.dtype) for e in ecs])
+    for e in ecs:
+        if e.num_cols != k or e.warp_size != w or e.delta_bits != b:
+            raise ValueError("stacked containers must share num_cols, warp_size and delta_bits")
+        for s in e.sets:
+            sets.append(EcCsrSet(s.granularity, s.vector_size, s.num_blocks, s.stored_cols,
+                                 s.real_nnz, np.asarray(s.row_indices, np.uint32) + np.uint32(off),
+                                 s.block_indptr, s.base_indices, s.delta_indices, s.pad_mask,
+                                 np.asarray(s.block_values, dtype)))
+        off += e.num_rows
+    return EcCsrMatrix(off, k, ecs[0].value_bits, b, w, sets)
+
+
+def to_f16(values: np.ndarray) -> np.ndarray:
+    """The packer's f32/f64 -> f16 rounding (IEEE RNE), for host-side parity checks."""
+    v = np.ascontiguousarray(values)
+    out = np.empty(v.shape, dtype=np.uint16)
+    _lib.check(_lib.lib().ecsr_b200_to_f16(v.ctypes.data, _lib.dtype_code(v.dtype),
+                                           out.ctypes.data, v.size), "ecsr_b200_to_f16")
+    return out.view(np.float16)

@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the reference's outputs and the oracle.
+
+Bars (north_star):
+  * encodings: unpack(pack(ec)) reproduces every reference array bit-exactly
+    (values: their fp16 rounding) -- tolerance 0;
+  * y, ordered mode: bitwise equal to the reference's f32 arithmetic on fp16-rounded
+    values and x (`y16`), and the generic f32/f64 handles bitwise equal to the
+    reference's compiled backend (`y32`, `y64`) -- tolerance 0;
+  * y, fast (atomic) mode: rel-inf <= 1e-5 vs y16 (only the y-accumulation order
+    differs) and rel-L2 <= 1e-3 vs the reference's FP32 result y32.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_names, load_golden, rel_err, rel_l2
+from paper_2507_12205_b200 import container as C
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2507_12205_b200 import backend  # noqa: E402
+from paper_2507_12205_b200.device import spmv, to_device, unpack, vstack  # noqa: E402
+
+TIGHT_ATOMIC = 1e-5
+NORTH_STAR_L2 = 1e-3
+
+
+def _x16(x):
+    return torch.from_numpy(x.astype(np.float16)).cuda()
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_f16_ordered_bitwise_and_atomic_tolerance(name):
+    g = load_golden(name)
+    ec, x = g["ec"], g["x"]
+    W = to_device(ec)
+    expect_tiled = ec.warp_size == 32 and ec.delta_bits <= 8 and len(ec.sets) > 0
+    assert (W.layout == "tiled") == expect_tiled
+    y_ord = spmv(W, _x16(x), ordered=True).cpu().numpy()
+    assert y_ord.dtype == np.float32
+    assert np.array_equal(y_ord, g["y16"]), rel_err(y_ord, g["y16"])
+    y_fast = spmv(W, _x16(x)).cpu().numpy()
+    assert rel_err(y_fast, g["y16"]) <= TIGHT_ATOMIC
+    assert rel_l2(y_fast, g["y32"]) <= NORTH_STAR_L2
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_generic_handles_bitwise_vs_reference_backend(name):
+    g = load_golden(name)
+    ec, x = g["ec"], g["x"]
+    W64 = to_device(ec, device_dtype="f64")
+    y64 = spmv(W64, torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(y64, g["y64"])
+    W32 = to_device(ec.astype(np.float32), device_dtype="f32")
+    y32 = spmv(W32, torch.from_numpy(x.astype(np.float32)).cuda()).cpu().numpy()
+    assert np.array_equal(y32, g["y32"])
+    W16g = to_device(ec, force_generic=True)
+    assert W16g.layout == "generic"
+    y16 = spmv(W16g, _x16(x)).cpu().numpy()
+    assert np.array_equal(y16, g["y16"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("force_generic", [False, True])
+def test_unpack_reproduces_encoding_bit_exactly(name, force_generic):
+    g = load_golden(name)
+    ec = g["ec"]
+    W = to_device(ec, force_generic=force_generic)
+    back = unpack(W, np.float64)
+    assert (back.num_rows, back.num_cols, back.warp_size, back.delta_bits) == (
+        ec.num_rows, ec.num_cols, ec.warp_size, ec.delta_bits)
+    assert len(back.sets) == len(ec.sets)
+    for a, b in zip(ec.sets, back.sets):
+        assert (a.granularity, a.vector_size, a.num_blocks, a.stored_cols, a.real_nnz) == (
+            b.granularity, b.vector_size, b.num_blocks, b.stored_cols, b.real_nnz)
+        for f in ("row_indices", "block_indptr", "base_indices", "delta_indices", "pad_mask"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        assert np.array_equal(a.block_values.astype(np.float16).astype(np.float64), b.block_values)
+    ec16 = ec.astype(np.float16).astype(np.float64)
+    assert C.serialize(back) == C.serialize(ec16)
+    assert C.storage_components(back, 16) == g["report"]
+    byt = W.bytes()
+    assert byt["model_kernel_bytes"] == C.kernel_model_bytes(ec)
+
+
+@pytest.mark.parametrize("name", ["uniform_256x256_s0.5_b8_seed11", "corpus_049",
+                                  "planted_512x384_s0.5_b8_seed15"])
+def test_accumulate_mode(name):
+    g = load_golden(name)
+    ec, x = g["ec"], g["x"]
+    W = to_device(ec)
+    y0 = np.random.default_rng(1).uniform(-1, 1, ec.num_rows).astype(np.float32)
+    y = torch.from_numpy(y0.copy()).cuda()
+    spmv(W, _x16(x), y=y, accumulate=True, ordered=True)
+    ec16 = ec.astype(np.float16).astype(np.float32)
+    ref = y0.copy()
+    for s in ec16.sets:
+        oracle.spmv_set(s.granularity, ec.warp_size, s.vector_size, s.row_indices,
+                        s.block_indptr, s.base_indices, s.delta_indices, s.block_values,
+                        x.astype(np.float16).astype(np.float32), ref)
+    assert np.array_equal(y.cpu().numpy(), ref)
+    y = torch.from_numpy(y0.copy()).cuda()
+    spmv(W, _x16(x), y=y, accumulate=True)
+    assert rel_err(y.cpu().numpy(), ref) <= TIGHT_ATOMIC
+
+
+@pytest.mark.parametrize("name", ["corpus_000", "corpus_049", "uniform_200x300_s0.7_b8_seed12",
+                                  "kat_two_row_block"])
+def test_backend_spmv_set_bitwise_vs_oracle(name):
+    g = load_golden(name)
+    ec, x = g["ec"], g["x"]
+    for dt in (np.float64, np.float32):
+        y_gpu = np.random.default_rng(2).uniform(-1, 1, ec.num_rows).astype(dt)
+        y_cpu = y_gpu.copy()
+        for s in ec.sets:
+            args = (s.granularity, ec.warp_size, s.vector_size, s.row_indices, s.block_indptr,
+                    s.base_indices, s.delta_indices, s.block_values.astype(dt), x.astype(dt))
+            backend.spmv_set(*args, y_gpu)
+            oracle.spmv_set(*args, y_cpu)
+        assert np.array_equal(y_gpu, y_cpu)
+
+
+def test_vstack_is_concatenation():
+    a = load_golden("uniform_256x256_s0.5_b8_seed11")
+    b = load_golden("uniform_256x256_s0.5_b4_seed17")
+    ec = vstack([a["ec"], b["ec"]]) if a["ec"].delta_bits == b["ec"].delta_bits else None
+    if ec is None:
+        ec = vstack([a["ec"], a["ec"]])
+        parts = [a, a]
+    else:
+        parts = [a, b]
+    x = a["x"]
+    W = to_device(ec)
+    y = spmv(W, _x16(x), ordered=True).cpu().numpy()
+    ec16 = ec.astype(np.float16).astype(np.float32)
+    ref = oracle.spmv_ec_oracle(ec16, x.astype(np.float16).astype(np.float32), np.float32)
+    assert np.array_equal(y, ref)
+    assert y.shape == (sum(p["ec"].num_rows for p in parts),)
+
+
+def test_empty_container_gives_zero():
+    ec = C.EcCsrMatrix(5, 7, 16, 8, 32, [])
+    W = to_device(ec)
+    y = spmv(W, torch.ones(7, dtype=torch.float16, device="cuda"))
+    assert torch.count_nonzero(y).item() == 0
+    y = spmv(W, torch.ones(7, dtype=torch.float16, device="cuda"), ordered=True)
+    assert torch.count_nonzero(y).item() == 0
+
+
+def test_zero_width_block_is_skipped():
+    # a hand-built set with a zero-width block between two real ones (_speedups.pyx:105-106)
+    g = load_golden("uniform_256x256_s0.5_b8_seed11")
+    ec = g["ec"]
+    s = ec.sets[0]
+    nb = s.num_blocks
+    indptr = np.concatenate([s.block_indptr[:2], s.block_indptr[1:]])
+    rows = np.concatenate([s.row_indices[:s.granularity], s.row_indices[:s.granularity],
+                           s.row_indices[s.granularity:]])
+    bases = np.concatenate([s.base_indices[:32], s.base_indices[:32], s.base_indices[32:]])
+    s2 = C.EcCsrSet(s.granularity, s.vector_size, nb + 1, s.stored_cols, s.real_nnz, rows,
+                    indptr, bases, s.delta_indices, s.pad_mask, s.block_values)
+    ec2 = C.EcCsrMatrix(ec.num_rows, ec.num_cols, ec.value_bits, ec.delta_bits, 32,
+                        [s2] + ec.sets[1:])
+    W = to_device(ec2)
+    y = spmv(W, _x16(g["x"]), ordered=True).cpu().numpy()
+    assert np.array_equal(y, g["y16"])
+    back = unpack(W, np.float64)
+    assert np.array_equal(back.sets[0].block_indptr, indptr)
+
+
+def test_cuda_graph_replay_and_determinism():
+    g = load_golden("planted_512x384_s0.5_b8_seed15")
+    W = to_device(g["ec"])
+    x = _x16(g["x"])
+    y = torch.empty(W.num_rows, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        spmv(W, x, y=y, ordered=True)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        spmv(W, x, y=y, ordered=True)
+    for _ in range(3):
+        y.fill_(7.0)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), g["y16"])
+
+
+def test_x_dtype_and_shape_errors():
+    g = load_golden("uniform_256x256_s0.5_b8_seed11")
+    W = to_device(g["ec"])
+    with pytest.raises(ValueError):
+        spmv(W, torch.ones(255, dtype=torch.float16, device="cuda"))
+    with pytest.raises(ValueError):
+        spmv(W, torch.ones(256, dtype=torch.float32, device="cuda"))
