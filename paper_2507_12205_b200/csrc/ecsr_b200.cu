@@ -10,8 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -36,7 +38,20 @@ int fail(int code, const std::string& msg) {
             return fail(ECSR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-constexpr int kTileTarget = 8192;       // bytes of whole blocks per tile (balance granularity)
+int tile_target() {  // bytes of whole blocks per tile (balance granularity); env override for tuning
+    static int v = [] {
+        const char* e = std::getenv("ECSR_B200_TILE");
+        return e ? std::max(1024, std::atoi(e)) : 32768;
+    }();
+    return v;
+}
+int debug_flags() {  // tuning experiments only: 1 = consumers skip compute, 2 = no y memset
+    static int v = [] {
+        const char* e = std::getenv("ECSR_B200_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
 constexpr int kMaxStageBytes = 65536;   // largest tile a ring slot may hold
 constexpr int kMaxStages = 16;
 constexpr int kPackInternal = 1 << 30;  // spmv_set: unbounded u32 deltas (validated by range)
@@ -131,6 +146,9 @@ struct ecsr_dev {
     uint32_t* d_tile_start16 = nullptr;
     int64_t ntiles = 0;
     uint32_t* d_cta_tile = nullptr;
+    uint32_t* d_tile_rec = nullptr;        // [ntiles + 1] record prefix counts
+    unsigned long long* d_sync = nullptr;  // zero-y grid-barrier generation counter
+    unsigned long long* d_trace = nullptr; // debug timeline (ECSR_B200_DEBUG & 4)
     int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
     // ordered reduction
     void* d_partials = nullptr;
@@ -217,12 +235,6 @@ int validate(const ecsr_host_set* sets, int nsets, int64_t M, int64_t K, int W, 
 
 bool pow2_le32(int g) { return g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32; }
 
-int tiled_header_bytes(int g) { return static_cast<int>(round_up(8 + 4 * g, 16)); }
-
-int64_t tiled_record_bytes(int g, int64_t n, bool wide) {
-    return tiled_header_bytes(g) + (wide ? 128 : 64) + n + 2 * g * n;
-}
-
 struct DeviceLimits {
     int sms = 148;
     int smem_optin = 232448;
@@ -234,75 +246,196 @@ int query_limits(int device, DeviceLimits* lim) {
     return ECSR_OK;
 }
 
-// Build the block-major tiled arena (record layout: ecsr_kernels.cuh, tiled_block).
-void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<SetDesc>& desc,
-                       int host_dtype, bool wide, std::vector<uint8_t>* arena,
-                       std::vector<uint32_t>* tile_start16, int64_t* max_tile) {
-    arena->clear();
-    tile_start16->clear();
-    *max_tile = 0;
-    std::vector<std::pair<int, int64_t>> cur;  // (set, block) of the open tile
-    int64_t cur_bytes = 0;                     // record bytes of the open tile
-    auto hdr_of = [](size_t nblk) { return round_up(4 + 2 * static_cast<int64_t>(nblk), 16); };
-    auto flush = [&]() {
-        if (cur.empty()) return;
-        const int64_t start = static_cast<int64_t>(arena->size());
-        const int64_t hdr = hdr_of(cur.size());
-        arena->resize(start + hdr + cur_bytes, 0);
-        uint8_t* base = arena->data() + start;
-        const uint32_t nblk = static_cast<uint32_t>(cur.size());
-        std::memcpy(base, &nblk, 4);
-        int64_t off = hdr;
-        for (size_t i = 0; i < cur.size(); ++i) {
-            const ecsr_host_set& s = sets[cur[i].first];
-            const SetDesc& d = desc[cur[i].first];
-            const int64_t b = cur[i].second;
-            const int g = s.granularity, v = s.vector_size;
-            const int64_t st = s.block_indptr[b], n = s.block_indptr[b + 1] - st;
-            const uint16_t off16 = static_cast<uint16_t>(off / 16);
-            std::memcpy(base + 4 + 2 * i, &off16, 2);
-            uint8_t* r = base + off;
-            const uint32_t slot0 = static_cast<uint32_t>(d.slot0 + b * g);
-            const uint16_t nchunk = static_cast<uint16_t>(n / (32 * v));
-            std::memcpy(r, &slot0, 4);
-            std::memcpy(r + 4, &nchunk, 2);
-            r[6] = static_cast<uint8_t>(g);
-            r[7] = static_cast<uint8_t>(v);
-            std::memcpy(r + 8, s.row_indices + b * g, 4 * g);
-            uint8_t* q = r + tiled_header_bytes(g);
-            for (int t = 0; t < 32; ++t) {
-                const uint32_t bv = s.base_indices[b * 32 + t];
-                if (wide) {
-                    std::memcpy(q + 4 * t, &bv, 4);
-                } else {
-                    const uint16_t b16 = static_cast<uint16_t>(bv);
-                    std::memcpy(q + 2 * t, &b16, 2);
-                }
+// ---------------------------------------------------------------------------------
+// Tiled device layout (read by ecsr_tiled_kernel; constants in ecsr_kernels.cuh).
+//
+// Blocks are grouped, in container order, into group records of P = 8 / g consecutive
+// blocks of one (g, v) run (P = 1 for g >= 8), so that one warp carries 8 row
+// accumulators and walks the P blocks' chunk streams interleaved with one pointer:
+//   [0, 32)  u32 slot[8]      ordered-mode partial slot of each block's row 0
+//   [32, 48) u16 ntail[8]     chunks beyond nmin, per block
+//   [48, 54) u16 nmin | u8 g | u8 v | u8 nblk | u8 present (bit b: block b has chunks)
+//   [64, ..) u32 rows[P][g]   | pad 16
+//   bases    per lane P entries (u16; u32 when K > 65535)
+//   nmin x [deltas_0..P-1 (32v each) | values_0..P-1 (64vg each)]
+//   tails    block 0's ntail[0] x [32v | 64vg], then block 1's, ...
+// Every 32v / 64vg span is exactly one chunk of the reference's chunk-permuted streams
+// (storage.py:147-181), so unpack restores the reference arrays bit-exactly. Missing
+// blocks of a short last record get zero chunks in the interleaved part (never emitted).
+// Records are packed into tiles of one (g, v) run:
+//   u32 nrec | u16 (g << 8 | v) | u16 0 | u16 rec_off16[nrec] | pad 16 | records
+// ---------------------------------------------------------------------------------
+struct GroupPlan {
+    std::vector<std::pair<int, int64_t>> blocks;  // (set, block), container order
+};
+
+int group_p(int g) { return g >= 8 ? 1 : 8 / g; }
+
+int64_t block_chunks(const ecsr_host_set& s, int64_t b) {
+    return (s.block_indptr[b + 1] - s.block_indptr[b]) / (32 * s.vector_size);
+}
+
+int64_t group_record_bytes(const ecsr_host_set* sets, const GroupPlan& gp, bool wide) {
+    const ecsr_host_set& s0 = sets[gp.blocks[0].first];
+    const int g = s0.granularity, v = s0.vector_size, P = group_p(g);
+    int64_t nmin = INT64_MAX, total = 0;
+    for (auto& sb : gp.blocks) {
+        const int64_t n = block_chunks(sets[sb.first], sb.second);
+        nmin = std::min(nmin, n);
+        total += n;
+    }
+    const int64_t chunk = 32 * v + 64 * v * g;
+    const int64_t tails = total - nmin * static_cast<int64_t>(gp.blocks.size());
+    return ecsr::group_header_bytes(g, P) + (wide ? 128 : 64) * P + chunk * (nmin * P + tails);
+}
+
+// Consumer-cycle estimate of one record on one SM (tile balancing): shared-memory
+// walks issue ~(3 + g) instructions per column per lane, ~4 per chunk for the
+// delta/value loads, ~150 per record for header, reduce-scatter and emit; an SM
+// issues ~2.4 warp instructions per cycle in practice. HBM delivers ~23.6 B per
+// cycle per SM at the measured peak, so a tile costs the sum of both estimates.
+double group_record_cost(const ecsr_host_set* sets, const GroupPlan& gp, bool wide) {
+    const ecsr_host_set& s0 = sets[gp.blocks[0].first];
+    const int g = s0.granularity, v = s0.vector_size;
+    double steps = 0;
+    for (auto& sb : gp.blocks) steps += static_cast<double>(block_chunks(sets[sb.first], sb.second));
+    const double instr = 150.0 + steps * (v * (3.0 + g) + 4.0);
+    return instr / 2.4 + static_cast<double>(group_record_bytes(sets, gp, wide)) / 23.6;
+}
+
+void write_group_record(const ecsr_host_set* sets, const std::vector<SetDesc>& desc, const GroupPlan& gp,
+                        int host_dtype, bool wide, uint8_t* r) {
+    const ecsr_host_set& s0 = sets[gp.blocks[0].first];
+    const int g = s0.granularity, v = s0.vector_size, P = group_p(g);
+    const int nb = static_cast<int>(gp.blocks.size());
+    std::vector<int64_t> nch(nb), st(nb);
+    int64_t nmin = INT64_MAX;
+    uint8_t present = 0;
+    for (int b = 0; b < nb; ++b) {
+        const ecsr_host_set& s = sets[gp.blocks[b].first];
+        nch[b] = block_chunks(s, gp.blocks[b].second);
+        st[b] = s.block_indptr[gp.blocks[b].second];
+        nmin = std::min(nmin, nch[b]);
+        if (nch[b] > 0) present |= static_cast<uint8_t>(1u << b);
+        const uint32_t slot = static_cast<uint32_t>(desc[gp.blocks[b].first].slot0 + gp.blocks[b].second * g);
+        std::memcpy(r + 4 * b, &slot, 4);
+    }
+    for (int b = 0; b < nb; ++b) {
+        const uint16_t t16 = static_cast<uint16_t>(nch[b] - nmin);
+        std::memcpy(r + 32 + 2 * b, &t16, 2);
+    }
+    const uint16_t nmin16 = static_cast<uint16_t>(nmin);
+    std::memcpy(r + 48, &nmin16, 2);
+    r[50] = static_cast<uint8_t>(g);
+    r[51] = static_cast<uint8_t>(v);
+    r[52] = static_cast<uint8_t>(nb);
+    r[53] = present;
+    for (int b = 0; b < nb; ++b)
+        std::memcpy(r + 64 + 4 * g * b, sets[gp.blocks[b].first].row_indices + gp.blocks[b].second * g, 4 * g);
+    uint8_t* q = r + ecsr::group_header_bytes(g, P);
+    const int esz = wide ? 4 : 2;
+    for (int t = 0; t < 32; ++t)
+        for (int b = 0; b < nb; ++b) {
+            const uint32_t bv = sets[gp.blocks[b].first].base_indices[gp.blocks[b].second * 32 + t];
+            if (wide) std::memcpy(q + (t * P + b) * esz, &bv, 4);
+            else {
+                const uint16_t b16 = static_cast<uint16_t>(bv);
+                std::memcpy(q + (t * P + b) * esz, &b16, 2);
             }
-            q += wide ? 128 : 64;
-            for (int64_t i2 = 0; i2 < n; ++i2) q[i2] = static_cast<uint8_t>(s.delta_indices[st + i2]);
-            q += n;
-            uint16_t* hv = reinterpret_cast<uint16_t*>(q);
-            for (int64_t i2 = 0; i2 < n * g; ++i2)
-                hv[i2] = f64_to_f16(host_value(s.block_values, host_dtype, st * g + i2));
-            off += tiled_record_bytes(g, n, wide);
         }
-        tile_start16->push_back(static_cast<uint32_t>(start / 16));
-        *max_tile = std::max<int64_t>(*max_tile, hdr + cur_bytes);
-        cur.clear();
-        cur_bytes = 0;
+    q += 32 * P * esz;
+    const int64_t dch = 32 * v, vch = 32 * v * g;  // per chunk: deltas (bytes), values (elements)
+    auto put_deltas = [&](int b, int64_t c) {
+        const ecsr_host_set& s = sets[gp.blocks[b].first];
+        for (int64_t i = 0; i < dch; ++i) q[i] = static_cast<uint8_t>(s.delta_indices[st[b] + c * dch + i]);
+        q += dch;
     };
-    for (int si = 0; si < nsets; ++si) {
-        const ecsr_host_set& s = sets[si];
-        for (int64_t b = 0; b < s.num_blocks; ++b) {
-            const int64_t n = s.block_indptr[b + 1] - s.block_indptr[b];
-            const int64_t rec = tiled_record_bytes(s.granularity, n, wide);
-            if (!cur.empty() && hdr_of(cur.size() + 1) + cur_bytes + rec > kTileTarget) flush();
-            cur.emplace_back(si, b);
-            cur_bytes += rec;
+    auto put_values = [&](int b, int64_t c) {
+        const ecsr_host_set& s = sets[gp.blocks[b].first];
+        uint16_t* hv = reinterpret_cast<uint16_t*>(q);
+        const int64_t v0 = (st[b] + c * dch) * g;
+        for (int64_t i = 0; i < vch; ++i) hv[i] = f64_to_f16(host_value(s.block_values, host_dtype, v0 + i));
+        q += 2 * vch;
+    };
+    for (int64_t c = 0; c < nmin; ++c) {
+        for (int b = 0; b < P; ++b) {
+            if (b < nb) put_deltas(b, c);
+            else q += dch;  // missing block: zero chunk
+        }
+        for (int b = 0; b < P; ++b) {
+            if (b < nb) put_values(b, c);
+            else q += 2 * vch;
         }
     }
-    flush();
+    for (int b = 0; b < nb; ++b)
+        for (int64_t c = nmin; c < nch[b]; ++c) {
+            put_deltas(b, c);
+            put_values(b, c);
+        }
+}
+
+// Build the tiled arena: group records in container order, tiles of one (g, v) run.
+void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<SetDesc>& desc,
+                       int host_dtype, bool wide, std::vector<uint8_t>* arena,
+                       std::vector<uint32_t>* tile_start16, std::vector<uint32_t>* tile_rec_start,
+                       std::vector<double>* tile_cost, int64_t* max_tile) {
+    arena->clear();
+    tile_start16->clear();
+    tile_rec_start->assign(1, 0u);
+    tile_cost->clear();
+    *max_tile = 0;
+    // 1. plan records: P consecutive blocks of a (g, v) run
+    std::vector<std::vector<GroupPlan>> runs;
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        const bool new_run = si == 0 || sets[si - 1].granularity != s.granularity ||
+                             sets[si - 1].vector_size != s.vector_size;
+        if (new_run) runs.emplace_back();
+        const int P = group_p(s.granularity);
+        for (int64_t b = 0; b < s.num_blocks; ++b) {
+            auto& run = runs.back();
+            if (run.empty() || static_cast<int>(run.back().blocks.size()) == P) run.emplace_back();
+            run.back().blocks.emplace_back(si, b);
+        }
+    }
+    // 2. pack records into tiles of <= tile_target() bytes
+    auto hdr_of = [](size_t n) { return round_up(8 + 2 * static_cast<int64_t>(n), 16); };
+    for (const auto& run : runs) {
+        size_t i = 0;
+        while (i < run.size()) {
+            size_t n = 0;
+            int64_t bytes = 0;
+            while (i + n < run.size()) {
+                const int64_t rb = round_up(group_record_bytes(sets, run[i + n], wide), 16);
+                if (n > 0 && hdr_of(n + 1) + bytes + rb > tile_target()) break;
+                bytes += rb;
+                ++n;
+            }
+            const int64_t start = static_cast<int64_t>(arena->size());
+            const int64_t hdr = hdr_of(n);
+            arena->resize(start + hdr + bytes, 0);
+            uint8_t* base = arena->data() + start;
+            const uint32_t nrec = static_cast<uint32_t>(n);
+            std::memcpy(base, &nrec, 4);
+            const ecsr_host_set& s0 = sets[run[i].blocks[0].first];
+            const uint16_t gv = static_cast<uint16_t>((s0.granularity << 8) | s0.vector_size);
+            std::memcpy(base + 4, &gv, 2);
+            int64_t off = hdr;
+            double cost = 0;
+            for (size_t k = 0; k < n; ++k) {
+                const uint16_t off16 = static_cast<uint16_t>(off / 16);
+                std::memcpy(base + 8 + 2 * k, &off16, 2);
+                write_group_record(sets, desc, run[i + k], host_dtype, wide, base + off);
+                off += round_up(group_record_bytes(sets, run[i + k], wide), 16);
+                cost += group_record_cost(sets, run[i + k], wide);
+            }
+            tile_start16->push_back(static_cast<uint32_t>(start / 16));
+            tile_rec_start->push_back(tile_rec_start->back() + static_cast<uint32_t>(n));
+            tile_cost->push_back(cost);
+            *max_tile = std::max<int64_t>(*max_tile, hdr + bytes);
+            i += n;
+        }
+    }
     tile_start16->push_back(static_cast<uint32_t>(arena->size() / 16));
 }
 
@@ -421,9 +554,7 @@ int configure_tiled_kernels(int smem) {
     static int configured = 0;
     std::lock_guard<std::mutex> lock(mu);
     if (configured >= smem) return ECSR_OK;
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true>,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
     return ECSR_OK;
@@ -566,17 +697,19 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                  delta_bits <= 8;
     for (int si = 0; si < nsets && tiled; ++si) {
         const int g = sets[si].granularity, v = sets[si].vector_size;
-        if (!pow2_le32(g) || !(v == 1 || v == 2 || v == 4 || v == 8)) tiled = false;
+        if (!pow2_le32(g) || !(v == 1 || v == 4)) tiled = false;  // kernel variants: v in {1, 4}
         for (int64_t b = 0; b < sets[si].num_blocks && tiled; ++b)
             if ((sets[si].block_indptr[b + 1] - sets[si].block_indptr[b]) / (32 * v) > 65535) tiled = false;
     }
     const bool wide = num_cols > 65535;
     if (tiled) {
         std::vector<uint8_t> arena;
-        std::vector<uint32_t> tstart;
+        std::vector<uint32_t> tstart, trec;
+        std::vector<double> tcost;
         int64_t max_tile = 0;
-        build_tiled_arena(sets, nsets, d->sets, host_value_dtype, wide, &arena, &tstart, &max_tile);
-        const int64_t stage = round_up(std::max<int64_t>(max_tile, kTileTarget), 128);
+        build_tiled_arena(sets, nsets, d->sets, host_value_dtype, wide, &arena, &tstart, &trec, &tcost,
+                          &max_tile);
+        const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
         const int64_t avail = lim.smem_optin - 1024 - 16 * kMaxStages - xbytes;
         const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
@@ -586,18 +719,20 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             d->wide = wide;
             d->stage_bytes = static_cast<int>(stage);
             d->nstages = static_cast<int>(nst);
-            d->smem_bytes = static_cast<int>(round_up(16 * nst, 128) + nst * stage + xbytes);
+            d->smem_bytes = static_cast<int>(round_up(16 * nst + 8, 128) + nst * stage + xbytes);
             const int64_t ntiles = static_cast<int64_t>(tstart.size()) - 1;
             d->ntiles = ntiles;
             const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(lim.sms, ntiles)));
             d->grid = grid;
-            // byte-balanced contiguous tile ranges
+            // cost-balanced contiguous tile ranges (HBM bytes + consumer issue estimate)
             std::vector<uint32_t> cta(grid + 1, 0);
-            const double total_bytes = static_cast<double>(arena.size());
+            std::vector<double> cum(ntiles + 1, 0.0);
+            for (int64_t t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + tcost[t];
+            const double total_cost = cum[ntiles];
             int c = 1;
             for (int64_t t = 0; t < ntiles && c < grid; ++t) {
-                const double mid = 16.0 * (0.5 * (static_cast<double>(tstart[t]) + tstart[t + 1]));
-                while (c < grid && mid >= total_bytes * c / grid) cta[c++] = static_cast<uint32_t>(t);
+                const double mid = 0.5 * (cum[t] + cum[t + 1]);
+                while (c < grid && mid >= total_cost * c / grid) cta[c++] = static_cast<uint32_t>(t);
             }
             while (c < grid) cta[c++] = static_cast<uint32_t>(ntiles);
             cta[grid] = static_cast<uint32_t>(ntiles);
@@ -613,6 +748,14 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             if (err == cudaSuccess) {
                 d->d_cta_tile = dalloc_copy(cta, &total, &err);
                 if (d->d_cta_tile) d->allocs.push_back(d->d_cta_tile);
+            }
+            if (err == cudaSuccess) {
+                d->d_tile_rec = dalloc_copy(trec, &total, &err);
+                if (d->d_tile_rec) d->allocs.push_back(d->d_tile_rec);
+            }
+            if (err == cudaSuccess) {
+                d->d_sync = dalloc_copy(std::vector<unsigned long long>(2, 0ull), &total, &err);
+                if (d->d_sync) d->allocs.push_back(d->d_sync);
             }
             if (err != cudaSuccess) {
                 delete d;
@@ -657,14 +800,13 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int accumulate = mode & ECSR_SPMV_ACCUMULATE;
     const bool ordered = (mode & ECSR_SPMV_ORDERED) != 0 || d->layout == 2;
-    const size_t ysize = d->dtype == ECSR_F64 ? 8 : 4;
     if (d->M == 0) return ECSR_OK;
     if (d->layout == 1) {
-        if (!ordered && !accumulate) ECSR_CUDA(cudaMemsetAsync(y, 0, d->M * ysize, st));
         ecsr::TiledParams p;
         p.arena = d->d_arena;
         p.tile_start16 = d->d_tile_start16;
         p.cta_tile = d->d_cta_tile;
+        p.tile_rec = d->d_tile_rec;
         p.x = static_cast<const __half*>(x);
         p.y = static_cast<float*>(y);
         p.partials = static_cast<float*>(d->d_partials);
@@ -673,13 +815,26 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
         p.stage_bytes = d->stage_bytes;
         p.nstages = d->nstages;
         p.x_vec16 = (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-        cudaError_t e;
-        if (d->wide)
-            e = launch_pdl(ecsr::ecsr_tiled_kernel<true>, dim3(d->grid), dim3(ecsr::kThreadsTiled),
-                           d->smem_bytes, st, p);
-        else
-            e = launch_pdl(ecsr::ecsr_tiled_kernel<false>, dim3(d->grid), dim3(ecsr::kThreadsTiled),
-                           d->smem_bytes, st, p);
+        p.debug = debug_flags();
+        p.sync = d->d_sync;
+        p.M = d->M;
+        p.zero_y = (!ordered && !accumulate) ? 1 : 0;
+        p.trace = nullptr;
+        if (debug_flags() & 4) {
+            ecsr_dev* dm = const_cast<ecsr_dev*>(d);
+            if (!dm->d_trace) {
+                ECSR_CUDA(cudaMalloc(&dm->d_trace, 8 * 16 * d->grid));
+                dm->allocs.push_back(dm->d_trace);
+            }
+            std::vector<unsigned long long> init(16 * d->grid, 0ull);
+            for (int c = 0; c < d->grid; ++c) init[16 * c + 7] = ~0ull;
+            ECSR_CUDA(cudaMemcpyAsync(dm->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice, st));
+            ECSR_CUDA(cudaStreamSynchronize(st));
+            p.trace = dm->d_trace;
+        }
+        p.wide = d->wide;
+        cudaError_t e = launch_pdl(ecsr::ecsr_tiled_kernel, dim3(d->grid), dim3(ecsr::kThreadsTiled),
+                                   d->smem_bytes, st, p);
         ECSR_CUDA(e);
         if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
         return ECSR_OK;
@@ -750,51 +905,68 @@ int ecsr_b200_unpack(const ecsr_dev* d, ecsr_out_set* out, int32_t nsets, int32_
             out[si].block_indptr[0] = 0;
             ++si;
         }
+        // Walk group records in order; every block restores its reference arrays.
         for (int64_t t = 0; t < d->ntiles; ++t) {
             const uint8_t* tile = arena.data() + 16ull * tstart[t];
-            uint32_t nblk;
-            std::memcpy(&nblk, tile, 4);
-            for (uint32_t j = 0; j < nblk; ++j) {
-                if (si >= nsets) return fail(ECSR_ERR_CONTAINER, "arena holds more blocks than sets");
-                const SetDesc& sd = d->sets[si];
-                ecsr_out_set& o = out[si];
+            uint32_t nrec;
+            std::memcpy(&nrec, tile, 4);
+            for (uint32_t jr = 0; jr < nrec; ++jr) {
                 uint16_t off16;
-                std::memcpy(&off16, tile + 4 + 2 * j, 2);
+                std::memcpy(&off16, tile + 8 + 2 * jr, 2);
                 const uint8_t* r = tile + 16 * off16;
-                uint16_t nchunk;
-                std::memcpy(&nchunk, r + 4, 2);
-                const int g = r[6], v = r[7];
-                if (g != sd.g || v != sd.v) return fail(ECSR_ERR_CONTAINER, "arena/set descriptor mismatch");
-                const int64_t n = static_cast<int64_t>(nchunk) * 32 * v;
-                if (b == 0) o.block_indptr[0] = 0;
-                o.block_indptr[b + 1] = o.block_indptr[b] + n;
-                std::memcpy(o.row_indices + b * g, r + 8, 4 * g);
-                const uint8_t* q = r + tiled_header_bytes(g);
-                for (int l = 0; l < 32; ++l) {
-                    if (d->wide) {
-                        std::memcpy(o.base_indices + b * 32 + l, q + 4 * l, 4);
-                    } else {
-                        uint16_t b16;
-                        std::memcpy(&b16, q + 2 * l, 2);
-                        o.base_indices[b * 32 + l] = b16;
+                uint16_t nmin;
+                std::memcpy(&nmin, r + 48, 2);
+                const int g = r[50], v = r[51], nb = r[52], P = group_p(g);
+                const int esz = d->wide ? 4 : 2;
+                const uint8_t* q = r + ecsr::group_header_bytes(g, P);
+                const uint8_t* body = q + 32 * P * esz;
+                const int64_t dch = 32 * v, vch = 32 * v * g;
+                const int64_t S = P * (dch + 2 * vch);
+                const uint8_t* tail = body + nmin * S;
+                for (int bk = 0; bk < nb; ++bk) {
+                    if (si >= nsets) return fail(ECSR_ERR_CONTAINER, "arena holds more blocks than sets");
+                    const SetDesc& sd = d->sets[si];
+                    ecsr_out_set& o = out[si];
+                    if (g != sd.g || v != sd.v) return fail(ECSR_ERR_CONTAINER, "arena/set descriptor mismatch");
+                    uint16_t nt;
+                    std::memcpy(&nt, r + 32 + 2 * bk, 2);
+                    const int64_t nch = nmin + nt;
+                    if (b == 0) o.block_indptr[0] = 0;
+                    o.block_indptr[b + 1] = o.block_indptr[b] + nch * dch;
+                    std::memcpy(o.row_indices + b * g, r + 64 + 4 * g * bk, 4 * g);
+                    for (int l = 0; l < 32; ++l) {
+                        uint32_t bv = 0;
+                        std::memcpy(&bv, q + (l * P + bk) * esz, esz);
+                        o.base_indices[b * 32 + l] = bv;
                     }
-                }
-                q += d->wide ? 128 : 64;
-                const int64_t st0 = o.block_indptr[b];
-                for (int64_t i = 0; i < n; ++i) o.delta_indices[st0 + i] = q[i];
-                q += n;
-                for (int64_t i = 0; i < n * g; ++i) {
-                    uint16_t h;
-                    std::memcpy(&h, q + 2 * i, 2);
-                    if (out_value_dtype == ECSR_F16) static_cast<uint16_t*>(o.block_values)[st0 * g + i] = h;
-                    else store_value(o.block_values, out_value_dtype, st0 * g + i, f16_to_f32(h));
-                }
-                if (++b == sd.nb) {
-                    b = 0;
-                    ++si;
-                    while (si < nsets && d->sets[si].nb == 0) {
-                        out[si].block_indptr[0] = 0;
+                    const int64_t st0 = o.block_indptr[b];
+                    for (int64_t c = 0; c < nch; ++c) {
+                        const uint8_t* dp;
+                        const uint8_t* vp;
+                        if (c < nmin) {
+                            dp = body + c * S + bk * dch;
+                            vp = body + c * S + P * dch + bk * 2 * vch;
+                        } else {
+                            dp = tail;
+                            vp = tail + dch;
+                            tail += dch + 2 * vch;
+                        }
+                        for (int64_t i = 0; i < dch; ++i) o.delta_indices[st0 + c * dch + i] = dp[i];
+                        for (int64_t i = 0; i < vch; ++i) {
+                            uint16_t h;
+                            std::memcpy(&h, vp + 2 * i, 2);
+                            const int64_t at = (st0 + c * dch) * g + i;
+                            if (out_value_dtype == ECSR_F16) static_cast<uint16_t*>(o.block_values)[at] = h;
+                            else store_value(o.block_values, out_value_dtype, at, f16_to_f32(h));
+                        }
+                    }
+                    if (++b == sd.nb) {
+                        b = 0;
                         ++si;
+                        while (si < nsets && d->sets[si].nb == 0) {
+                            out[si].block_indptr[0] = 0;
+                            ++si;
+                        }
                     }
                 }
             }
@@ -838,6 +1010,14 @@ int ecsr_b200_bytes(const ecsr_dev* d, ecsr_bytes* out) {
 }
 
 void ecsr_b200_free(ecsr_dev* d) { delete d; }
+
+// Internal tuning aid (not part of the public header): the last traced launch's
+// per-CTA timeline, 8 u64 globaltimer stamps per CTA (ECSR_B200_DEBUG & 4).
+int ecsr_b200_debug_trace(const ecsr_dev* d, unsigned long long* out, int64_t n) {
+    if (!d || !d->d_trace) return fail(ECSR_ERR_VALUE, "no trace recorded");
+    ECSR_CUDA(cudaMemcpy(out, d->d_trace, 8 * std::min<int64_t>(n, 16 * d->grid), cudaMemcpyDeviceToHost));
+    return ECSR_OK;
+}
 
 int ecsr_b200_spmv_set(int32_t g, int32_t warp_size, int32_t vector_size, int64_t num_blocks,
                        const uint32_t* row_ids, const int64_t* block_indptr,

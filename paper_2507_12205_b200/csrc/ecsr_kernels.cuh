@@ -34,14 +34,19 @@
 
 namespace ecsr {
 
-constexpr int kNumConsumerWarps = 12;
+#ifndef ECSR_NCONS
+#define ECSR_NCONS 16
+#endif
+constexpr int kNumConsumerWarps = ECSR_NCONS;
 constexpr int kThreadsTiled = 32 * (kNumConsumerWarps + 1);
 constexpr int kProducerWarp = kNumConsumerWarps;
+constexpr int kMaxRingStages = 16;
 
 struct TiledParams {
     const uint8_t* arena;          // block-major tiles, 16-B aligned
     const uint32_t* tile_start16;  // [ntiles + 1] tile offsets in 16-B units
     const uint32_t* cta_tile;      // [grid + 1] first tile of each CTA
+    const uint32_t* tile_rec;      // [ntiles + 1] record prefix counts
     const __half* x;               // [K]
     float* y;                      // [M]
     float* partials;               // [nslots] (ordered mode)
@@ -49,7 +54,13 @@ struct TiledParams {
     int32_t ordered;
     int32_t stage_bytes;
     int32_t nstages;
+    unsigned long long* sync;      // grid-barrier generation counter (zero_y mode)
+    int64_t M;
     int32_t x_vec16;               // x is 16-B aligned
+    int32_t zero_y;                // overwrite: the kernel zeroes y itself (no memset launch)
+    int32_t wide;                  // K > 65535: u32 bases (else u16)
+    int32_t debug;                 // tuning experiments (ECSR_B200_DEBUG)
+    unsigned long long* trace;     // debug timeline [grid][8] (globaltimer ns) or null
 };
 
 // ---------------------------------------------------------------------------------
@@ -84,6 +95,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -98,6 +114,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define ECSR_TRACE(slot, cond)                                                       \
+    do {                                                                             \
+        if (p.trace && (cond)) p.trace[blockIdx.x * 16 + (slot)] = gtimer();        \
+    } while (0)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -132,43 +157,50 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&acc)[G], int lane) 
     return acc[0];
 }
 
-// Load `Bytes` (power of two, >= 2) from 16-B-aligned-enough shared memory into regs.
+// Load `Bytes` (power of two) from shared memory (32-bit shared address) into regs.
 template <int Bytes>
-__device__ __forceinline__ void lds_bytes(const uint8_t* p, uint32_t* r) {
+__device__ __forceinline__ void lds_bytes(uint32_t addr, uint32_t* r) {
     if constexpr (Bytes >= 16) {
 #pragma unroll
-        for (int i = 0; i < Bytes / 16; ++i) {
-            const uint4 v = reinterpret_cast<const uint4*>(p)[i];
-            r[4 * i + 0] = v.x;
-            r[4 * i + 1] = v.y;
-            r[4 * i + 2] = v.z;
-            r[4 * i + 3] = v.w;
-        }
+        for (int i = 0; i < Bytes / 16; ++i)
+            asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(r[4 * i]), "=r"(r[4 * i + 1]), "=r"(r[4 * i + 2]), "=r"(r[4 * i + 3])
+                         : "r"(addr + 16 * i));
     } else if constexpr (Bytes == 8) {
-        const uint2 v = *reinterpret_cast<const uint2*>(p);
-        r[0] = v.x;
-        r[1] = v.y;
+        asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
     } else if constexpr (Bytes == 4) {
-        r[0] = *reinterpret_cast<const uint32_t*>(p);
+        asm("ld.shared.u32 %0, [%1];" : "=r"(r[0]) : "r"(addr));
     } else if constexpr (Bytes == 2) {
-        r[0] = *reinterpret_cast<const uint16_t*>(p);
+        asm("ld.shared.u16 %0, [%1];" : "=r"(r[0]) : "r"(addr));
     } else {
-        r[0] = *p;
+        asm("ld.shared.u8 %0, [%1];" : "=r"(r[0]) : "r"(addr));
     }
 }
 
-__device__ __forceinline__ float half_lo(uint32_t w) {
-    return __half2float(__ushort_as_half(static_cast<unsigned short>(w & 0xffffu)));
-}
-__device__ __forceinline__ float half_hi(uint32_t w) {
-    return __half2float(__ushort_as_half(static_cast<unsigned short>(w >> 16)));
-}
-template <int N>
-__device__ __forceinline__ float half_at(const uint32_t (&r)[N], int i) {
-    return (i & 1) ? half_hi(r[i >> 1]) : half_lo(r[i >> 1]);
+__device__ __forceinline__ unsigned short lds_h(uint32_t addr) {
+    unsigned short h;
+    asm("ld.shared.b16 %0, [%1];" : "=h"(h) : "r"(addr));
+    return h;
 }
 
-// Block record (packer: ecsr_b200.cu, build_tiled_layout):
+// Mixed-precision FMA (sm_100a FHFMA): acc + a*b with f16 a, b and f32 acc, rounded
+// once. An f16 x f16 product is exact in f32, so this equals the reference's unfused
+// `res += val * x` in f32 (_speedups.pyx:119 under -ffp-contract=off, pkg/setup.py:26).
+__device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float acc) {
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(a), "h"(b));
+    return acc;
+}
+
+template <int N>
+__device__ __forceinline__ unsigned short half_at(const uint32_t (&r)[N], int i) {
+    unsigned short lo, hi;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(lo), "=h"(hi) : "r"(r[i >> 1]));
+    return (i & 1) ? hi : lo;
+}
+
+// Tile (packer: ecsr_b200.cu, build_tiled_arena), 16-B aligned, homogeneous in (g, v):
+//   u32 nblk | u8 g | u8 v | u16 0 | u16 block_off16[nblk] | pad to 16 | records
+// Block record:
 //   u32 slot0 | u16 nchunk | u8 g | u8 v | u32 rows[g] | pad to 16
 //   | bases[32] (u16, or u32 when WIDE) | u8 deltas[n] | f16 values[g*n]
 // deltas and values keep the reference's chunk permutation (storage.py:147-181):
@@ -179,135 +211,253 @@ __host__ __device__ constexpr int header_bytes() {
     return (8 + 4 * G + 15) & ~15;
 }
 
-template <int G, int V, bool WIDE>
-__device__ __forceinline__ void tiled_block(const uint8_t* __restrict__ blk,
-                                            const __half* __restrict__ xs, int lane,
-                                            const TiledParams& p) {
-    const uint32_t slot0 = *reinterpret_cast<const uint32_t*>(blk);
-    const uint32_t nchunk = *reinterpret_cast<const uint16_t*>(blk + 4);
-    const uint32_t* rows = reinterpret_cast<const uint32_t*>(blk + 8);
-    const uint8_t* q = blk + header_bytes<G>();
-    uint32_t idx = WIDE ? reinterpret_cast<const uint32_t*>(q)[lane]
-                        : static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(q)[lane]);
-    q += WIDE ? 128 : 64;
-    const uint8_t* dl = q + lane * V;
-    const uint8_t* vl = q + nchunk * (32 * V) + lane * (2 * V * G);
-    const unsigned short* xsu = reinterpret_cast<const unsigned short*>(xs);
-
-    float acc[G];
-#pragma unroll
-    for (int k = 0; k < G; ++k) acc[k] = 0.0f;
-
-    constexpr int kValBytes = 2 * V * G;       // per lane per chunk
-    constexpr bool kWhole = kValBytes <= 64;   // load a lane's chunk at once
-#pragma unroll 2
-    for (uint32_t c = 0; c < nchunk; ++c) {
-        uint32_t d[(V + 3) / 4];
-        lds_bytes<V>(dl + c * (32 * V), d);
-        if constexpr (kWhole) {
-            uint32_t w[(kValBytes + 3) / 4];
-            lds_bytes<kValBytes>(vl + c * (32 * kValBytes), w);
-#pragma unroll
-            for (int j = 0; j < V; ++j) {
-                idx += (d[j >> 2] >> (8 * (j & 3))) & 0xffu;
-                const float xv = __half2float(__ushort_as_half(xsu[idx]));
-#pragma unroll
-                for (int k = 0; k < G; ++k) acc[k] = fmaf(half_at(w, j * G + k), xv, acc[k]);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < V; ++j) {
-                idx += (d[j >> 2] >> (8 * (j & 3))) & 0xffu;
-                const float xv = __half2float(__ushort_as_half(xsu[idx]));
-                uint32_t w[G / 2];
-                lds_bytes<2 * G>(vl + c * (32 * kValBytes) + j * 2 * G, w);
-#pragma unroll
-                for (int k = 0; k < G; ++k) acc[k] = fmaf(half_at(w, k), xv, acc[k]);
-            }
+// Per-warp state of the zero-y grid barrier: REDs into y may only start once every
+// CTA has zeroed its slice of y (see ecsr_tiled_kernel).
+struct YGate {
+    const unsigned long long* counter;
+    unsigned long long target;
+    bool open;
+    __device__ __forceinline__ void pass(int lane) {
+        if (open) return;
+        if (lane == 0) {
+            unsigned long long v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+            } while (static_cast<long long>(v - target) < 0);
         }
+        __syncwarp();
+        open = true;
     }
-    if (nchunk == 0) return;  // zero-width blocks contribute nothing (_speedups.pyx:105-106)
-    const float sum = warp_reduce_scatter<G>(acc, lane);
-    constexpr int kStride = 32 / G;
-    if ((lane & (kStride - 1)) == 0) {
-        const int k = lane / kStride;
-        if (p.ordered) {
-            p.partials[slot0 + k] = sum;
-        } else {
-            atomicAdd(p.y + rows[k], sum);  // RED.E.ADD.F32 (result unused)
-        }
+};
+
+// Group records (packer: ecsr_b200.cu, build_tiled_arena / write_group_record): P = 8/g
+// consecutive blocks (P = 1 for g >= 8) whose chunk streams are interleaved, so a warp
+// carries 8 row accumulators and P independent column walks.
+constexpr int kAccPerWarp = 8;
+__host__ __device__ constexpr int group_header_bytes(int g, int P) { return 64 + ((4 * g * P + 15) & ~15); }
+
+template <int V>
+__device__ __forceinline__ void load_deltas(uint32_t addr, uint32_t (&d)[(V + 3) / 4]) {
+    lds_bytes<V>(addr, d);
+}
+
+// One chunk of one block on one lane: V columns, G rows each. Lane t's running column
+// index advances by its deltas exactly like _speedups.pyx:112-119; products go into
+// the block's G accumulators in the reference order.
+template <int G, int V, int NW>
+__device__ __forceinline__ void chunk_fma(const uint32_t (&d)[(V + 3) / 4], const uint32_t (&w)[NW],
+                                          uint32_t& xa, float* acc) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        xa += 2u * __byte_perm(d[j >> 2], 0u, 0x4440u + (j & 3));
+#ifdef ECSR_EXP_NOGATHER
+        const unsigned short xh = lds_h((xa & 0xfffu) | 0x100u);
+#else
+        const unsigned short xh = lds_h(xa);
+#endif
+#pragma unroll
+        for (int k = 0; k < G; ++k) acc[k] = fhfma(half_at(w, j * G + k), xh, acc[k]);
     }
 }
 
-template <bool WIDE>
-__device__ __forceinline__ void tiled_dispatch(const uint8_t* blk, const __half* xs, int lane,
-                                               const TiledParams& p) {
-    const uint32_t g = blk[6], v = blk[7];
-#define ECSR_CASE(GG, VV)                          \
-    case (GG << 4) | VV:                           \
-        tiled_block<GG, VV, WIDE>(blk, xs, lane, p); \
-        break;
-    switch ((g << 4) | v) {
-        ECSR_CASE(1, 4)
-        ECSR_CASE(2, 4)
-        ECSR_CASE(4, 4)
-        ECSR_CASE(8, 4)
-        ECSR_CASE(16, 4)
-        ECSR_CASE(1, 1)
-        ECSR_CASE(2, 1)
-        ECSR_CASE(4, 1)
-        ECSR_CASE(8, 1)
-        ECSR_CASE(16, 1)
-        ECSR_CASE(1, 2)
-        ECSR_CASE(2, 2)
-        ECSR_CASE(4, 2)
-        ECSR_CASE(8, 2)
-        ECSR_CASE(16, 2)
-        ECSR_CASE(1, 8)
-        ECSR_CASE(2, 8)
-        ECSR_CASE(4, 8)
-        ECSR_CASE(8, 8)
-        ECSR_CASE(16, 8)
-        ECSR_CASE(32, 1)
-        ECSR_CASE(32, 2)
-        ECSR_CASE(32, 4)
-        ECSR_CASE(32, 8)
-        default:
-            break;  // packer guarantees a supported (g, v)
+// Emit one row sum: red.global.add.f32 into y (fast) or the block's partial slot
+// (ordered; summed per row in container order by ecsr_finish_rows).
+__device__ __forceinline__ void emit_row(uint32_t r, int g, int P, int blk, int k, float sum,
+                                         const TiledParams& p) {
+    if (p.ordered) {
+        uint32_t slot;
+        lds_bytes<4>(r + 4 * blk, &slot);
+        asm volatile("st.global.f32 [%0], %1;" ::"l"(p.partials + slot + k), "f"(sum) : "memory");
+    } else {
+        uint32_t row;
+        lds_bytes<4>(r + 64 + 4 * (blk * g + k), &row);
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p.y + row), "f"(sum) : "memory");
     }
-#undef ECSR_CASE
 }
 
-template <bool WIDE>
-__global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const TiledParams p) {
+// One group record, g = G <= 8: P = 8/G blocks walked together. Per block, lane t
+// accumulates its segment sequentially (reference order); the 8 accumulators then
+// share one butterfly reduce-scatter whose per-accumulator association is the
+// reference's lane tree (_speedups.pyx:120-127).
+template <int G, int V>
+__device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const TiledParams& p,
+                                                   YGate& gate) {
+    constexpr int P = kAccPerWarp / G;
+    uint32_t m[2];
+    lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
+    const uint32_t nmin = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
+    if (!present) return;  // zero-width blocks only (_speedups.pyx:105-106)
+    uint32_t tl[(P + 1) / 2];
+    lds_bytes<2 * P>(r + 32, tl);  // ntail[P]
+    const uint32_t q = r + group_header_bytes(G, P);
+    uint32_t xa[P];
+    if (p.wide) {
+        uint32_t bb[P];
+        lds_bytes<4 * P>(q + lane * 4 * P, bb);
+#pragma unroll
+        for (int b = 0; b < P; ++b) xa[b] = xs + 2u * bb[b];
+    } else {
+        uint32_t bb[(P + 1) / 2];
+        lds_bytes<2 * P>(q + lane * 2 * P, bb);
+#pragma unroll
+        for (int b = 0; b < P; ++b) xa[b] = xs + 2u * ((bb[b >> 1] >> (16 * (b & 1))) & 0xffffu);
+    }
+    constexpr uint32_t DCH = 32 * V, VCH = 64 * V * G, LV = 2 * V * G;  // bytes
+    constexpr int NW = (LV + 3) / 4;
+    uint32_t ptr = q + (p.wide ? 128u : 64u) * P;
+    float acc[kAccPerWarp];
+#pragma unroll
+    for (int k = 0; k < kAccPerWarp; ++k) acc[k] = 0.0f;
+#pragma unroll 1
+    for (uint32_t c = 0; c < nmin; ++c, ptr += P * (DCH + VCH)) {
+        uint32_t d[P][(V + 3) / 4], w[P][NW];
+#pragma unroll
+        for (int b = 0; b < P; ++b) load_deltas<V>(ptr + b * DCH + lane * V, d[b]);
+#pragma unroll
+        for (int b = 0; b < P; ++b) lds_bytes<LV>(ptr + P * DCH + b * VCH + lane * LV, w[b]);
+#pragma unroll
+        for (int b = 0; b < P; ++b) chunk_fma<G, V, NW>(d[b], w[b], xa[b], acc + b * G);
+    }
+#pragma unroll
+    for (int b = 0; b < P; ++b) {  // tails: chunks beyond nmin, block after block
+        const uint32_t nt = (tl[b >> 1] >> (16 * (b & 1))) & 0xffffu;
+#pragma unroll 1
+        for (uint32_t c = 0; c < nt; ++c, ptr += DCH + VCH) {
+            uint32_t d[(V + 3) / 4], w[NW];
+            load_deltas<V>(ptr + lane * V, d);
+            lds_bytes<LV>(ptr + DCH + lane * LV, w);
+            chunk_fma<G, V, NW>(d, w, xa[b], acc + b * G);
+        }
+    }
+    const float sum = warp_reduce_scatter<kAccPerWarp>(acc, lane);
+    if (!p.ordered) gate.pass(lane);
+    const int a = lane >> 2;  // accumulator a: block a / G, row a % G
+    const int blk = a / G, k = a % G;
+    if ((lane & 3) == 0 && ((present >> blk) & 1u)) emit_row(r, G, P, blk, k, sum, p);
+}
+
+// A single-block record of g = 8 * passes rows (g in {16, 32}): one walk per pass of
+// 8 rows; a column's g values are contiguous, so a pass reads one 16-byte slice.
+template <int V>
+__device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs, int lane,
+                                                  const TiledParams& p, YGate& gate) {
+    constexpr int G = 8;
+    uint32_t m[2];
+    lds_bytes<8>(r + 48, m);
+    const uint32_t nch = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
+    if (!present) return;
+    const uint32_t q = r + group_header_bytes(g, 1);
+    uint32_t base;
+    if (p.wide) lds_bytes<4>(q + lane * 4, &base);
+    else {
+        lds_bytes<2>(q + lane * 2, &base);
+        base &= 0xffffu;
+    }
+    constexpr uint32_t DCH = 32 * V;
+    const uint32_t vch = 64u * V * g;
+    const uint32_t body = q + (p.wide ? 128u : 64u);
+    for (int pass = 0; pass < g / G; ++pass) {
+        uint32_t xa = xs + 2u * base;
+        float acc[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) acc[k] = 0.0f;
+        uint32_t ptr = body;
+#pragma unroll 1
+        for (uint32_t c = 0; c < nch; ++c, ptr += DCH + vch) {
+            uint32_t d[(V + 3) / 4];
+            load_deltas<V>(ptr + lane * V, d);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                xa += 2u * __byte_perm(d[j >> 2], 0u, 0x4440u + (j & 3));
+                const unsigned short xh = lds_h(xa);
+                uint32_t w[4];
+                lds_bytes<16>(ptr + DCH + (lane * V + j) * 2u * g + 16u * pass, w);
+#pragma unroll
+                for (int k = 0; k < G; ++k) acc[k] = fhfma(half_at(w, k), xh, acc[k]);
+            }
+        }
+        const float sum = warp_reduce_scatter<G>(acc, lane);
+        if (!p.ordered) gate.pass(lane);
+        if ((lane & 3) == 0) emit_row(r, g, 1, 0, (lane >> 2) + G * pass, sum, p);
+    }
+}
+
+__device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t xs, int lane,
+                                             const TiledParams& p, YGate& gate) {
+    const int g = static_cast<int>(gv >> 8);
+    const bool v4 = (gv & 0xffu) == 4;
+    if (g == 1) {
+        if (v4) tiled_group_record<1, 4>(r, xs, lane, p, gate);
+        else tiled_group_record<1, 1>(r, xs, lane, p, gate);
+    } else if (g == 2) {
+        if (v4) tiled_group_record<2, 4>(r, xs, lane, p, gate);
+        else tiled_group_record<2, 1>(r, xs, lane, p, gate);
+    } else if (g == 4) {
+        if (v4) tiled_group_record<4, 4>(r, xs, lane, p, gate);
+        else tiled_group_record<4, 1>(r, xs, lane, p, gate);
+    } else if (g == 8) {
+        if (v4) tiled_group_record<8, 4>(r, xs, lane, p, gate);
+        else tiled_group_record<8, 1>(r, xs, lane, p, gate);
+    } else {  // 16, 32: passes of 8 rows
+        if (v4) tiled_wide_record<4>(r, g, xs, lane, p, gate);
+        else tiled_wide_record<1>(r, g, xs, lane, p, gate);
+    }
+}
+
+// Persistent grid, one CTA per SM, warp-specialised:
+//   * producer warp (one elected lane): streams this CTA's byte-balanced tile range
+//     HBM -> shared memory with cp.async.bulk into an mbarrier ring, L2 evict_first;
+//     it starts before griddepcontrol.wait because the weights never depend on the
+//     previous kernel (PDL overlap of weight streaming with the predecessor's tail);
+//   * consumer warps: wait for the predecessor (x producer), stage x (fp16) in shared
+//     memory, then decode blocks from the ring.
+// Overwrite without a memset launch (zero_y): every CTA zeroes its slice of y, then
+// bumps a 64-bit generation counter; warps pass the gate (counter reached the
+// generation's multiple of gridDim.x) before their first red.global. PDL dependents
+// are released only after the arrival, so back-to-back launches of one handle never
+// interleave their generations.
+__global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + p.nstages;
-    uint8_t* stages = smem + ((16 * p.nstages + 127) & ~127);
+    uint64_t* xbar = empty + p.nstages;  // x staged (bulk copy or consumer copy)
+    uint8_t* stages = smem + ((16 * p.nstages + 8 + 127) & ~127);
     __half* xs = reinterpret_cast<__half*>(stages + p.nstages * p.stage_bytes);
+    __shared__ unsigned long long gate_target;
+    __shared__ uint32_t rec_next;                   // dynamic record scheduler
+    __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per ring stage
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t t0 = p.cta_tile[blockIdx.x];
     const uint32_t t1 = p.cta_tile[blockIdx.x + 1];
+    // x by one bulk copy when it is 16-B aligned and a multiple of 16 bytes
+    const bool x_bulk = p.x_vec16 && (p.K & 7) == 0 && p.K > 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.nstages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kNumConsumerWarps);
+            mbar_init(&empty[s], 1);  // the last finisher of a tile's records arrives
+            stage_done[s] = 0;
         }
+        mbar_init(xbar, 1);
+        rec_next = 0;
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_trigger();
+    ECSR_TRACE(0, threadIdx.x == 0);
 
     if (warp == kProducerWarp) {
-        // Weights do not depend on the previous kernel: stream them before pdl_wait.
+        if (!p.zero_y) pdl_trigger();
         if (lane == 0) {
             const uint64_t policy = l2_evict_first_policy();
             int stage = 0;
             uint32_t phase = 0;
-            for (uint32_t t = t0; t < t1; ++t) {
+            uint32_t t = t0;
+            // One tile goes out before x: it never depends on the predecessor kernel.
+            // The rest waits until x has landed, so the x request is not queued behind
+            // this SM's whole weight stream in the memory system.
+            auto issue = [&]() {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
                 const uint32_t bytes = (b - a) * 16u;
@@ -318,44 +468,115 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const Tile
                     stage = 0;
                     phase ^= 1u;
                 }
+                ++t;
+            };
+            if (t < t1) issue();
+            if (x_bulk) {
+                pdl_wait();
+                const uint32_t xbytes = static_cast<uint32_t>(p.K) * 2u;
+                mbar_arrive_expect_tx(xbar, xbytes);
+                bulk_g2s(xs, p.x, xbytes, xbar, l2_evict_last_policy());
             }
+            mbar_wait(xbar, 0);
+            while (t < t1) issue();
+            ECSR_TRACE(5, true);
         }
         return;
     }
 
-    // Consumers: x (the previous kernel's output) -> shared memory, once per CTA.
+    // Consumers: wait for the predecessor (x producer; y may alias its inputs).
     pdl_wait();
-    {
-        const int tid = threadIdx.x;
-        const int nthr = kNumConsumerWarps * 32;
-        if (p.x_vec16) {
-            const int nvec = p.K >> 3;
-            const uint4* src = reinterpret_cast<const uint4*>(p.x);
-            uint4* dst = reinterpret_cast<uint4*>(xs);
-            for (int i = tid; i < nvec; i += nthr) dst[i] = __ldg(src + i);
-            for (int i = (nvec << 3) + tid; i < p.K; i += nthr) xs[i] = p.x[i];
-        } else {
-            for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
+    ECSR_TRACE(1, threadIdx.x == 0);
+    const int tid = threadIdx.x;
+    constexpr int nthr = kNumConsumerWarps * 32;
+    if (p.zero_y) {
+        const int64_t r0 = p.M * blockIdx.x / gridDim.x, r1 = p.M * (blockIdx.x + 1) / gridDim.x;
+        for (int64_t r = r0 + tid; r < r1; r += nthr) p.y[r] = 0.0f;
+        __threadfence();
+    }
+    if (!x_bulk) {
+        for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
+        consumer_bar_sync();
+        if (tid == 0) mbar_arrive(xbar);
+    }
+    YGate gate{p.sync, 0ull, !p.zero_y};
+    if (p.zero_y) {
+        consumer_bar_sync();
+        if (tid == 0) {
+            unsigned long long old;
+            asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.sync) : "memory");
+            gate_target = old - old % gridDim.x + gridDim.x;
+        }
+        consumer_bar_sync();
+        gate.target = gate_target;
+        pdl_trigger();
+    }
+    mbar_wait(xbar, 0);
+    ECSR_TRACE(2, threadIdx.x == 0);
+
+    const uint32_t xs_addr = smem_addr(xs);
+    const uint32_t stages_addr = smem_addr(stages);
+    // Dynamic scheduling: warps take the CTA's records in container order from a
+    // shared counter (balances unequal records); the last warp to finish a tile's
+    // records releases its ring stage to the producer.
+    const uint32_t rec0 = p.tile_rec[t0];
+    const uint32_t nrec_cta = p.tile_rec[t1] - rec0;
+    uint32_t ti = 0;                       // tile cursor (relative to t0)
+    uint32_t tile_end = p.tile_rec[t0 + 1] - rec0;
+    uint32_t tile_begin = 0;
+#ifdef ECSR_TRACE_CYCLES
+    unsigned long long cyc_wait = 0, cyc_work = 0, nwork = 0;
+#endif
+    while (true) {
+        uint32_t k = 0;
+        if (lane == 0) k = atomicAdd(&rec_next, 1u);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= nrec_cta) break;
+        while (k >= tile_end) {
+            ++ti;
+            tile_begin = tile_end;
+            tile_end = p.tile_rec[t0 + ti + 1] - rec0;
+        }
+        const uint32_t stage = ti % p.nstages;
+#ifdef ECSR_TRACE_CYCLES
+        const unsigned long long c0 = clock64();
+#endif
+        mbar_wait(&full[stage], (ti / p.nstages) & 1u);
+#ifdef ECSR_TRACE_CYCLES
+        const unsigned long long c1 = clock64();
+        cyc_wait += c1 - c0;
+#endif
+        ECSR_TRACE(3, threadIdx.x == 0 && ti == 0);
+        const uint32_t tile = stages_addr + stage * p.stage_bytes;
+        uint32_t th[2];
+        lds_bytes<8>(tile, th);
+        const uint32_t gv = th[1] & 0xffffu;
+        uint32_t off16;
+        lds_bytes<2>(tile + 8 + 2 * (k - tile_begin), &off16);
+        if (!(p.debug & 1)) tiled_record(tile + 16u * off16, gv, xs_addr, lane, p, gate);
+#ifdef ECSR_TRACE_CYCLES
+        cyc_work += clock64() - c1;
+        ++nwork;
+#endif
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t done = atomicAdd(&stage_done[stage], 1u) + 1u;
+            if (done == th[0]) {  // all records of this tile finished: release the stage
+                stage_done[stage] = 0;
+                mbar_arrive(&empty[stage]);
+            }
         }
     }
-    consumer_bar_sync();
-
-    int stage = 0;
-    uint32_t phase = 0;
-    uint32_t j = static_cast<uint32_t>(warp);  // round-robin block index across the CTA range
-    for (uint32_t t = t0; t < t1; ++t) {
-        mbar_wait(&full[stage], phase);
-        const uint8_t* tile = stages + stage * p.stage_bytes;
-        const uint32_t nblk = *reinterpret_cast<const uint32_t*>(tile);
-        const uint16_t* offs = reinterpret_cast<const uint16_t*>(tile + 4);
-        for (; j < nblk; j += kNumConsumerWarps) tiled_dispatch<WIDE>(tile + offs[j] * 16u, xs, lane, p);
-        j -= nblk;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == p.nstages) {
-            stage = 0;
-            phase ^= 1u;
-        }
+    ECSR_TRACE(4, threadIdx.x == 0);
+    if (p.trace && lane == 0) {
+        atomicMax(p.trace + blockIdx.x * 16 + 6, gtimer());
+        atomicMin(p.trace + blockIdx.x * 16 + 7, gtimer());
+#ifdef ECSR_TRACE_CYCLES
+        atomicAdd(p.trace + blockIdx.x * 16 + 8, cyc_wait);
+        atomicAdd(p.trace + blockIdx.x * 16 + 9, cyc_work);
+        atomicAdd(p.trace + blockIdx.x * 16 + 10, nwork);
+#endif
+        atomicAdd(p.trace + blockIdx.x * 16 + 11, static_cast<unsigned long long>(t1 - t0));
     }
 }
 

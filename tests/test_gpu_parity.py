@@ -199,3 +199,28 @@ def test_x_dtype_and_shape_errors():
         spmv(W, torch.ones(255, dtype=torch.float16, device="cuda"))
     with pytest.raises(ValueError):
         spmv(W, torch.ones(256, dtype=torch.float32, device="cuda"))
+
+
+@pytest.mark.parametrize("name", ["planted_512x384_s0.5_b8_seed15", "magnitude_256x512_s0.7_b8_seed14"])
+def test_overwrite_mode_zeroes_y_in_kernel_across_graph_replays(name):
+    # fast overwrite: the kernel zeroes y itself behind a generation-counted grid gate;
+    # back-to-back launches of one handle (same stream, PDL) must never see stale y.
+    g = load_golden(name)
+    W = to_device(g["ec"])
+    x = _x16(g["x"])
+    ys = [torch.full((W.num_rows,), 1e6, dtype=torch.float32, device="cuda") for _ in range(3)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        spmv(W, x, y=ys[0])
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        for y in ys:
+            spmv(W, x, y=y)
+    for rep in range(4):
+        for y in ys:
+            y.fill_(-3e5 * (rep + 1))
+        graph.replay()
+        torch.cuda.synchronize()
+        for y in ys:
+            assert rel_err(y.cpu().numpy(), g["y16"]) <= TIGHT_ATOMIC
