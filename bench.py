@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""bench.py -- EC-CSR batch-1 SpMV hot path on B200 (BASELINE.json configs[1]).
+
+Workload ("llama7b-layer-s0.5"): the seven SpMVs of one LLaMA-7B decoder layer at 50 %
+per-row magnitude pruning (random N(0, 1/K) weights, seeded), encoded to EC-CSR by the
+reference pipeline (W=32, V=4, B=8; `convert_csr`, cached as .ecsr under cache/):
+q, k, v, o 4096x4096, gate, up 11008x4096, down 4096x11008. One step = the layer's
+SpMVs as 4 stream-ordered launches (q|k|v and gate|up row-stacked, because they share
+x; o; down), each y = W x with fp16 values and x, fp32 accumulate and y.
+
+Reported (one JSON line, rank 0):
+  value        algorithmic GB/s = model bytes per step / device time per step, with
+               everything resident in HBM; model bytes = storage_report(value_bits=16)
+               components minus pad_mask/desc + 2K (x) + 4M (y) per matrix (SURVEY.md
+               §8(d)); the 284 MB per step exceed the 126 MB L2, so no flush is needed.
+  e2e          same metric through the public device API with pinned-host x copied in
+               and y copied out every step (H2D/D2H inside the timed region).
+  roofline     the tiled kernel's per-launch algorithmic bytes / its CUDA-event time,
+               against the measured HBM copy peak (MEASURED_PEAKS.json, else the
+               6.65 TB/s fallback of /opt/skills/guides/B200_PROFILING.md).
+  cpu_baseline the reference's own compiled kernel (oracle/_ref/_speedups*.so, built from
+               the reference's _speedups.pyx) driven like executor.spmv_ec, one core, on a
+               bounded sample of the same workload.
+
+`--impl reference` runs only the reference CPU path (all host cores: one process per
+matrix of the layer) on the same workload and prints its line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOAD = "llama7b-layer-s0.5"
+# (name, generator, rows, cols, sparsity, seed, input)
+MATRICES = [
+    ("q", "magnitude", 4096, 4096, 0.5, 101, "x_attn"),
+    ("k", "magnitude", 4096, 4096, 0.5, 102, "x_attn"),
+    ("v", "magnitude", 4096, 4096, 0.5, 103, "x_attn"),
+    ("o", "magnitude", 4096, 4096, 0.5, 104, "x_o"),
+    ("gate", "magnitude", 11008, 4096, 0.5, 105, "x_mlp"),
+    ("up", "magnitude", 11008, 4096, 0.5, 106, "x_mlp"),
+    ("down", "magnitude", 4096, 11008, 0.5, 107, "x_down"),
+]
+# launches per step: matrices sharing an input are row-stacked into one container
+LAUNCHES = [("qkv", ["q", "k", "v"]), ("o", ["o"]), ("gate_up", ["gate", "up"]), ("down", ["down"])]
+FALLBACK_HBM_GBS = 6650.0
+METRIC = "SpMV latency (µs) and achieved HBM GB/s vs B200 roofline; speedup vs CPU ref"
+
+
+def cache_path(name):
+    m = {n: (g, r, c, s, sd) for n, g, r, c, s, sd, _ in MATRICES}[name]
+    g, r, c, s, sd = m
+    return os.path.join(ROOT, "cache", f"{g}_{r}x{c}_s{s}_seed{sd}.ecsr")
+
+
+def load_workload():
+    """EC-CSR encodings of the layer: cache/*.ecsr when present (scripts/make_cache.sh:
+    the reference's convert_csr), else the native encoder, which is byte-identical to
+    the reference (tests/test_encoder.py), writing the cache for the next run."""
+    from paper_2507_12205_b200.container import load_container, save_container
+    from paper_2507_12205_b200.encoder import convert_csr
+    from paper_2507_12205_b200.generators import make_matrix
+
+    ecs, sources = {}, set()
+    for name, kind, rows, cols, s, seed, _ in MATRICES:
+        path = cache_path(name)
+        if os.path.exists(path):
+            ecs[name] = load_container(path)
+            sources.add("cache")
+            continue
+        ecs[name] = convert_csr(make_matrix(kind, rows, cols, s, seed, dtype=np.float32))
+        sources.add("native-encoder")
+        try:
+            os.makedirs(os.path.dirname(path), exist_ok=True)
+            save_container(ecs[name], path + ".tmp")
+            os.replace(path + ".tmp", path)
+        except OSError:
+            pass
+    return ecs, sorted(sources)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        for key in ("hbm_gbs", "hbm_GBps", "hbm"):
+            if key in d:
+                return float(d[key]), "measured"
+    except (OSError, ValueError):
+        pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(
+        os.environ.get("WORLD_SIZE", 1))
+
+
+def model_bytes(ecs):
+    from paper_2507_12205_b200.container import kernel_model_bytes
+
+    return {n: kernel_model_bytes(ec) for n, ec in ecs.items()}
+
+
+# ------------------------------------------------------------------------------------
+# CPU reference path (oracle/_ref: the reference's compiled kernel), test/bench only
+# ------------------------------------------------------------------------------------
+
+def _ref_set_fn():
+    import oracle
+
+    ref = oracle.load_reference_speedups()
+    if ref is not None:
+        return ref.spmv_set, "reference"
+    return oracle.spmv_set, "port"
+
+
+def _cpu_spmv_once(name, reps):
+    """Worker: reps x executor.spmv_ec(ec_f32, x_f32, validate=False) on one matrix."""
+    import oracle
+
+    from paper_2507_12205_b200.container import load_container
+
+    ec = load_container(cache_path(name)).astype(np.float32)
+    x = np.random.default_rng(5000).uniform(-1, 1, ec.num_cols).astype(np.float32)
+    fn, kind = _ref_set_fn()
+    oracle.spmv_ec_oracle(ec, x, np.float32, set_fn=fn)  # warm-up (cli.py:235-240 method)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.spmv_ec_oracle(ec, x, np.float32, set_fn=fn)
+    return (time.perf_counter() - t0) / reps, kind
+
+
+def cpu_baseline(mbytes, budget_s=10.0):
+    """One core, the reference kernel, the whole layer repeated for ~budget_s."""
+    per = {}
+    kind = "reference"
+    for name, *_ in MATRICES:
+        t, kind = _cpu_spmv_once(name, 1)
+        per[name] = t
+    layer = sum(per.values())
+    reps = max(1, int(budget_s / max(layer, 1e-6)))
+    per = {}
+    for name, *_ in MATRICES:
+        t, kind = _cpu_spmv_once(name, reps)
+        per[name] = t
+    layer = sum(per.values())
+    total = sum(mbytes.values())
+    return {"value": round(total / layer / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": kind,
+            "sample": f"{reps} x the full layer (7 SpMVs, {total / 1e6:.1f} MB model bytes), "
+                      f"{layer * 1e3:.1f} ms per layer on 1 of {os.cpu_count()} cores",
+            "ms_per_step": round(layer * 1e3, 3),
+            "us_per_spmv": {k: round(v * 1e6, 1) for k, v in per.items()}}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    ecs, _ = load_workload()
+    mbytes = model_bytes(ecs)
+    del ecs
+    names = [m[0] for m in MATRICES]
+    procs = min(len(names), os.cpu_count() or 1)
+    # one warm-up step, then K timed steps; each step = the layer's 7 SpMVs, one process
+    # per matrix (the reference kernel is single-threaded, GIL held: _speedups.pyx:81-129)
+    with mp.get_context("spawn").Pool(procs) as pool:
+        pool.starmap(_cpu_spmv_once, [(n, 1) for n in names])
+        t0 = time.perf_counter()
+        res = pool.starmap(_cpu_spmv_once, [(n, args.steps) for n in names])
+        wall = time.perf_counter() - t0
+    kind = res[0][1]
+    step_s = max(t for t, _ in res)  # steps run concurrently per matrix
+    total = sum(mbytes.values())
+    value = total / step_s / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "matrices": [m[:6] for m in MATRICES],
+                   "encoder": "reference convert_csr W=32 V=4 B=8", "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": procs, "kind": kind,
+                         "sample": f"{args.steps} steps x 7 SpMVs, one process per matrix, "
+                                   f"wall {wall:.1f}s"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------
+# GPU path
+# ------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2507_12205_b200 import to_device
+    from paper_2507_12205_b200.device import spmv, vstack
+
+    ecs, sources = load_workload()
+    mbytes = model_bytes(ecs)
+    step_bytes = sum(mbytes.values())
+    launch_bytes = {ln: sum(mbytes[n] for n in names) for ln, names in LAUNCHES}
+    handles = {ln: to_device(vstack([ecs[n] for n in names])) for ln, names in LAUNCHES}
+    layout = {ln: W.bytes() for ln, W in handles.items()}
+    inputs = {"qkv": "x_attn", "o": "x_o", "gate_up": "x_mlp", "down": "x_down"}
+    kdim = {"qkv": 4096, "o": 4096, "gate_up": 4096, "down": 11008}
+    rng = np.random.default_rng(5000 + rank)
+    xs_host = {ln: torch.from_numpy(rng.uniform(-1, 1, kdim[ln]).astype(np.float16)).pin_memory()
+               for ln, _ in LAUNCHES}
+    xs = {ln: xs_host[ln].to(dev) for ln in xs_host}
+    ys = {ln: torch.empty(handles[ln].num_rows, dtype=torch.float32, device=dev) for ln in handles}
+    ys_host = {ln: torch.empty(ys[ln].shape, dtype=torch.float32).pin_memory() for ln in ys}
+    stream = torch.cuda.Stream(dev)
+
+    def step():
+        for ln, _ in LAUNCHES:
+            spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
+
+    # correctness guard (cheap): o = W_o x_o against the CPU oracle on this rank's data
+    with torch.cuda.stream(stream):
+        step()
+    torch.cuda.synchronize()
+    import oracle
+
+    ec16 = ecs["o"].astype(np.float16).astype(np.float32)
+    ref = oracle.spmv_ec_oracle(ec16, xs_host["o"].numpy().astype(np.float32), np.float32)
+    got = ys["o"].cpu().numpy()
+    rel = float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30))
+    if rel > 1e-5:
+        raise SystemExit(f"parity guard failed: rel-inf {rel:.3e}")
+
+    # device-resident timing: CUDA graph of one step, replayed
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            step()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+
+    # per-launch kernel durations (roofline of the dominant kernel), same stream
+    ev = {ln: [] for ln, _ in LAUNCHES}
+    reps = max(args.steps, 10)
+    for _ in range(reps):
+        for ln, _ in LAUNCHES:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
+            b.record(stream)
+            ev[ln].append((a, b))
+    torch.cuda.synchronize()
+    launch_ms = {ln: statistics.median(a.elapsed_time(b) for a, b in ev[ln]) for ln in ev}
+
+    # end-to-end through the public API: pinned host x in, y out, every step
+    h2d = sum(x.numel() * 2 for x in xs_host.values())
+    d2h = sum(y.numel() * 4 for y in ys_host.values())
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            for ln, _ in LAUNCHES:
+                xs[ln].copy_(xs_host[ln], non_blocking=True)
+            step()
+            for ln, _ in LAUNCHES:
+                ys_host[ln].copy_(ys[ln], non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = t.tolist()
+    if rank != 0:
+        return
+    peak, peak_kind = peaks()
+    kernel_ms = sum(launch_ms.values())
+    achieved = step_bytes / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_step")
+    line = {
+        "metric": METRIC,
+        "value": round(world * step_bytes / (ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 values/x, f32 accumulate", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "matrices": [m[:6] for m in MATRICES],
+                   "launches_per_step": [ln for ln, _ in LAUNCHES],
+                   "model_bytes_per_step": step_bytes,
+                   "l2": "inputs 284 MB/step > 126 MB L2 (no flush)",
+                   "encoder": "convert_csr W=32 V=4 B=8 (" + "+".join(sources) + ")",
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "latency_us": {ln: round(v * 1e3, 2) for ln, v in launch_ms.items()},
+        "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+                "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel",
+                     "device_arena_bytes": {ln: layout[ln]["device_arena_bytes"] for ln in layout}},
+        "gpu_launches": len(LAUNCHES) * args.steps,
+        "clocks": clocks.summary(),
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(mbytes, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -137,6 +137,25 @@ int ecsr_b200_spmv_set(int32_t g, int32_t warp_size, int32_t vector_size, int64_
                        const void* block_values, const void* x, int64_t x_len, void* y,
                        int64_t y_len, int32_t y_dtype);
 
+/* ---- Native encoder (host, OpenMP): bit-exact with the reference's offline pipeline
+ * storage.convert_csr (storage.py:700-708 -> extraction.py:153-356, balance.py:10-55,
+ * storage.py:99-251). Replaces the reference's O(M^2 K)-per-round numpy encoder.
+ * Input: CSR with strictly increasing columns per row (core.py:24-57); values f32/f64.
+ * max_levels < 0 = None, clip_limit < 0 = None (automatic threshold), threads <= 0 =
+ * OpenMP default. Output sets are read with ecsr_b200_enc_set_info / _copy_set (the
+ * same arrays as ecsr.storage.EcCsrSet; ecsr_out_set buffers sized from the info). */
+typedef struct ecsr_enc ecsr_enc;
+int ecsr_b200_encode(int64_t num_rows, int64_t num_cols, const int64_t* row_ptr,
+                     const int64_t* col_idx, const void* values, int32_t value_dtype,
+                     int32_t warp_size, int32_t vector_size, int32_t delta_bits,
+                     int32_t max_levels, int64_t clip_limit, int32_t threads, ecsr_enc** out);
+int ecsr_b200_enc_nsets(const ecsr_enc* enc);
+int ecsr_b200_enc_set_info(const ecsr_enc* enc, int32_t set, ecsr_set_info* info);
+int ecsr_b200_enc_copy_set(const ecsr_enc* enc, int32_t set, ecsr_out_set* out,
+                           int32_t out_value_dtype);
+void ecsr_b200_enc_free(ecsr_enc* enc);
+const char* ecsr_b200_enc_last_error(void);
+
 /* IEEE round-to-nearest-even conversion used by pack (exposed for tests). */
 int ecsr_b200_to_f16(const void* src, int32_t src_dtype, uint16_t* dst, int64_t n);
 

@@ -73,6 +73,13 @@ SIGNATURES = {
     "ecsr_b200_spmv_set": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_i64, c_i32]),
     "ecsr_b200_to_f16": (c_i32, [c_vp, c_i32, c_vp, c_i64]),
+    "ecsr_b200_encode": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                 c_i64, c_i32, ctypes.POINTER(c_vp)]),
+    "ecsr_b200_enc_nsets": (c_i32, [c_vp]),
+    "ecsr_b200_enc_set_info": (c_i32, [c_vp, c_i32, ctypes.POINTER(SetInfo)]),
+    "ecsr_b200_enc_copy_set": (c_i32, [c_vp, c_i32, ctypes.POINTER(OutSet), c_i32]),
+    "ecsr_b200_enc_free": (None, [c_vp]),
+    "ecsr_b200_enc_last_error": (ctypes.c_char_p, []),
     "ecsr_b200_last_error": (ctypes.c_char_p, []),
     "ecsr_b200_version": (ctypes.c_char_p, []),
     "ecsr_b200_device_count": (c_i32, []),

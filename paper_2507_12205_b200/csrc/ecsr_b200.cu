@@ -269,7 +269,7 @@ struct GroupPlan {
     std::vector<std::pair<int, int64_t>> blocks;  // (set, block), container order
 };
 
-int group_p(int g) { return g >= 8 ? 1 : 8 / g; }
+int group_p(int g) { return g > 8 ? 1 : ecsr::group_blocks(g); }
 
 int64_t block_chunks(const ecsr_host_set& s, int64_t b) {
     return (s.block_indptr[b + 1] - s.block_indptr[b]) / (32 * s.vector_size);

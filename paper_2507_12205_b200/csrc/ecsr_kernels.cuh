@@ -233,7 +233,11 @@ struct YGate {
 // Group records (packer: ecsr_b200.cu, build_tiled_arena / write_group_record): P = 8/g
 // consecutive blocks (P = 1 for g >= 8) whose chunk streams are interleaved, so a warp
 // carries 8 row accumulators and P independent column walks.
-constexpr int kAccPerWarp = 8;
+#ifndef ECSR_ACC
+#define ECSR_ACC 8
+#endif
+constexpr int kAccPerWarp = ECSR_ACC;  // row accumulators per warp in a group record
+__host__ __device__ constexpr int group_blocks(int g) { return g >= kAccPerWarp ? 1 : kAccPerWarp / g; }
 __host__ __device__ constexpr int group_header_bytes(int g, int P) { return 64 + ((4 * g * P + 15) & ~15); }
 
 template <int V>
@@ -282,7 +286,8 @@ __device__ __forceinline__ void emit_row(uint32_t r, int g, int P, int blk, int 
 template <int G, int V>
 __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const TiledParams& p,
                                                    YGate& gate) {
-    constexpr int P = kAccPerWarp / G;
+    constexpr int P = group_blocks(G);
+    constexpr int NACC = P * G;
     uint32_t m[2];
     lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
     const uint32_t nmin = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
@@ -305,16 +310,24 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
     constexpr uint32_t DCH = 32 * V, VCH = 64 * V * G, LV = 2 * V * G;  // bytes
     constexpr int NW = (LV + 3) / 4;
     uint32_t ptr = q + (p.wide ? 128u : 64u) * P;
-    float acc[kAccPerWarp];
+    float acc[NACC];
 #pragma unroll
-    for (int k = 0; k < kAccPerWarp; ++k) acc[k] = 0.0f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0f;
 #pragma unroll 1
     for (uint32_t c = 0; c < nmin; ++c, ptr += P * (DCH + VCH)) {
         uint32_t d[P][(V + 3) / 4], w[P][NW];
+#ifdef ECSR_EXP_NOWEIGHTLDS
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+            for (int i = 0; i < (V + 3) / 4; ++i) d[b][i] = 0x01010101u + (c & 1);
+            for (int i = 0; i < NW; ++i) w[b][i] = 0x3c003c00u ^ (c << 3);
+        }
+#else
 #pragma unroll
         for (int b = 0; b < P; ++b) load_deltas<V>(ptr + b * DCH + lane * V, d[b]);
 #pragma unroll
         for (int b = 0; b < P; ++b) lds_bytes<LV>(ptr + P * DCH + b * VCH + lane * LV, w[b]);
+#endif
 #pragma unroll
         for (int b = 0; b < P; ++b) chunk_fma<G, V, NW>(d[b], w[b], xa[b], acc + b * G);
     }
@@ -329,11 +342,12 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
             chunk_fma<G, V, NW>(d, w, xa[b], acc + b * G);
         }
     }
-    const float sum = warp_reduce_scatter<kAccPerWarp>(acc, lane);
+    const float sum = warp_reduce_scatter<NACC>(acc, lane);
     if (!p.ordered) gate.pass(lane);
-    const int a = lane >> 2;  // accumulator a: block a / G, row a % G
+    constexpr int kStride = 32 / NACC;
+    const int a = lane / kStride;  // accumulator a: block a / G, row a % G
     const int blk = a / G, k = a % G;
-    if ((lane & 3) == 0 && ((present >> blk) & 1u)) emit_row(r, G, P, blk, k, sum, p);
+    if ((lane & (kStride - 1)) == 0 && ((present >> blk) & 1u)) emit_row(r, G, P, blk, k, sum, p);
 }
 
 // A single-block record of g = 8 * passes rows (g in {16, 32}): one walk per pass of

@@ -46,6 +46,10 @@ def main():
     ok = n > 0
     print(f"  per pair (cycles): header {np.sum(t[ok, 12]) / n[ok].sum():.0f}  loop {np.sum(t[ok, 13]) / n[ok].sum():.0f}"
           f" (chunk-steps/pair {ch[ok].sum() / n[ok].sum():.2f})  reduce+emit {np.sum(t[ok, 14]) / n[ok].sum():.0f}; pairs/CTA {np.median(n):.0f}")
+    if os.environ.get("TRACE_PER_CTA"):
+        ld = (t[:, 4] - t0) / 1e3
+        for c0 in range(0, grid, 8):
+            print("   cta", c0, " ".join(f"{v:5.2f}" for v in ld[c0:c0 + 8]), " tiles", t[c0:c0 + 8, 11] // 16)
     hot = np.argsort(-t[:, 9])[:5]
     print("  slowest CTAs (work us):", [(int(c), round(float(k[c]), 2)) for c in hot])
 
