@@ -440,6 +440,9 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
     __shared__ unsigned long long gate_target;
     __shared__ uint32_t rec_next;                   // dynamic record scheduler
     __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per ring stage
+    // tile (relative to t0) the producer last put in each stage: a warp may be handed a
+    // record several ring cycles ahead, and an mbarrier parity wait alone would alias
+    __shared__ uint32_t stage_tile[kMaxRingStages];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -453,6 +456,7 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);  // the last finisher of a tile's records arrives
             stage_done[s] = 0;
+            stage_tile[s] = 0xffffffffu;
         }
         mbar_init(xbar, 1);
         rec_next = 0;
@@ -475,6 +479,9 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
                 mbar_wait(&empty[stage], phase ^ 1u);
                 const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
                 const uint32_t bytes = (b - a) * 16u;
+                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_tile[stage])),
+                             "r"(t - t0)
+                             : "memory");
                 mbar_arrive_expect_tx(&full[stage], bytes);
                 bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a) * 16u,
                          bytes, &full[stage], policy);
@@ -555,6 +562,12 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c0 = clock64();
 #endif
+        {  // wait until the producer has put tile ti in this stage, then for its bytes
+            uint32_t cur;
+            do {
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(cur) : "r"(smem_addr(&stage_tile[stage])) : "memory");
+            } while (cur != ti);
+        }
         mbar_wait(&full[stage], (ti / p.nstages) & 1u);
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c1 = clock64();

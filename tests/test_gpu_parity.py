@@ -224,3 +224,35 @@ def test_overwrite_mode_zeroes_y_in_kernel_across_graph_replays(name):
         torch.cuda.synchronize()
         for y in ys:
             assert rel_err(y.cpu().numpy(), g["y16"]) <= TIGHT_ATOMIC
+
+
+@pytest.mark.parametrize("tile", ["4096", "8192"])
+def test_ring_wraps_many_times_small_tiles(tile, monkeypatch):
+    # records handed out several ring cycles ahead of the producer (regression: parity
+    # aliasing of the full barriers); the tile size is read once per process, so run a
+    # child process with a small ECSR_B200_TILE
+    import subprocess
+    import sys as _sys
+
+    code = (
+        "import numpy as np, torch, oracle;"
+        "from conftest import load_golden;"
+        "from paper_2507_12205_b200.device import spmv, to_device, vstack;"
+        "g = load_golden('planted_512x384_s0.5_b8_seed15');"
+        "ec = vstack([g['ec']] * 6); W = to_device(ec);"
+        "assert W.bytes()['tiles'] > 8 * W.bytes()['stages'];"
+        "x = g['x'];"
+        "y = spmv(W, torch.from_numpy(x.astype(np.float16)).cuda(), ordered=True).cpu().numpy();"
+        "ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),"
+        " x.astype(np.float16).astype(np.float32), np.float32);"
+        "assert np.array_equal(y, ref);"
+        "[spmv(W, torch.from_numpy(x.astype(np.float16)).cuda()) for _ in range(20)];"
+        "torch.cuda.synchronize(); print('ok')"
+    )
+    import os as _os
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    env = dict(_os.environ, ECSR_B200_TILE=tile,
+               PYTHONPATH=_os.pathsep.join([root, _os.path.join(root, "tests")]))
+    out = subprocess.run([_sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
