@@ -317,8 +317,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     with torch.cuda.graph(graph, stream=stream):
         step()
-    for _ in range(args.warmup):
-        graph.replay()
+    with torch.cuda.stream(stream):  # replay() launches on the current stream
+        for _ in range(args.warmup):
+            graph.replay()
     torch.cuda.synchronize()
 
     def barrier():
@@ -330,7 +331,7 @@ def run_ours(args):
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(local_rank) as clocks, torch.cuda.stream(stream):
         e0.record(stream)
         for _ in range(args.steps):
             graph.replay()
@@ -338,40 +339,59 @@ def run_ours(args):
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
 
-    # per-launch kernel durations (roofline of the dominant kernel), same stream
-    ev = {ln: [] for ln, _ in LAUNCHES}
-    reps = max(args.steps, 10)
-    for _ in range(reps):
-        for ln, _ in LAUNCHES:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+    # per-launch device time of each launch kind: a graph of that launch alone, replayed
+    # (CUDA events on the launching stream; its weights, > L2 together with the other
+    # launches' between replays, are re-streamed from HBM: evict-first L2 policy)
+    launch_ms = {}
+    for ln, _ in LAUNCHES:
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=stream):
             spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
-            b.record(stream)
-            ev[ln].append((a, b))
-    torch.cuda.synchronize()
-    launch_ms = {ln: statistics.median(a.elapsed_time(b) for a, b in ev[ln]) for ln in ev}
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                g1.replay()
+                graph.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tot = 0.0
+            for _ in range(max(5, args.steps // 2)):
+                graph.replay()  # flush: the whole layer (284 MB) streams through L2
+                a.record(stream)
+                g1.replay()
+                b.record(stream)
+                b.synchronize()
+                tot += a.elapsed_time(b)
+        launch_ms[ln] = tot / max(5, args.steps // 2)
 
     # end-to-end through the public API: pinned host x in, y out, every step
     h2d = sum(x.numel() * 2 for x in xs_host.values())
     d2h = sum(y.numel() * 4 for y in ys_host.values())
 
-    def e2e_step():
-        with torch.cuda.stream(stream):
-            for ln, _ in LAUNCHES:
-                xs[ln].copy_(xs_host[ln], non_blocking=True)
-            step()
-            for ln, _ in LAUNCHES:
-                ys_host[ln].copy_(ys[ln], non_blocking=True)
+    def e2e_body():
+        for ln, _ in LAUNCHES:
+            xs[ln].copy_(xs_host[ln], non_blocking=True)
+        step()
+        for ln, _ in LAUNCHES:
+            ys_host[ln].copy_(ys[ln], non_blocking=True)
 
-    for _ in range(args.warmup):
-        e2e_step()
+    # the same step with its host<->device copies, captured once (pinned-host memcpy
+    # nodes + the 4 launches) so the host API overhead does not dominate 100 us steps
+    g_e2e = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_e2e, stream=stream):
+        e2e_body()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            g_e2e.replay()
     barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(stream)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            g_e2e.replay()
+        e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps
+    # the copies really happened: the host y of the o launch matches the device one
+    if not torch.equal(ys_host["o"], ys["o"].cpu()):
+        raise SystemExit("e2e graph did not copy y back to the host")
 
     if world > 1:
         import torch.distributed as dist
@@ -382,8 +402,10 @@ def run_ours(args):
     if rank != 0:
         return
     peak, peak_kind = peaks()
-    kernel_ms = sum(launch_ms.values())
-    achieved = step_bytes / (kernel_ms * 1e-3) / 1e9
+    # dominant (only) kernel: every launch of the step is ecsr_tiled_kernel, so its average
+    # launch duration over the timed region is ms / launches and the algorithmic bytes of
+    # a launch average step_bytes / launches
+    achieved = step_bytes / (ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
