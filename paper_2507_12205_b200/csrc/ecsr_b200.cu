@@ -711,7 +711,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                           &max_tile);
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
-        const int64_t avail = lim.smem_optin - 1024 - 16 * kMaxStages - xbytes;
+        const int64_t avail = lim.smem_optin - 3072 - 16 * kMaxStages - xbytes;  // static smem + barriers
         const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
         if (stage > kMaxStageBytes || nst < 2 || arena.size() / 16 >= (1ull << 32)) tiled = false;
         if (tiled) {

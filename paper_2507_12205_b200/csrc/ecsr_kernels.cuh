@@ -41,6 +41,7 @@ constexpr int kNumConsumerWarps = ECSR_NCONS;
 constexpr int kThreadsTiled = 32 * (kNumConsumerWarps + 1);
 constexpr int kProducerWarp = kNumConsumerWarps;
 constexpr int kMaxRingStages = 16;
+constexpr uint32_t kTileRecCache = 256;  // per-CTA record prefix counts kept in smem
 
 struct TiledParams {
     const uint8_t* arena;          // block-major tiles, 16-B aligned
@@ -213,17 +214,24 @@ __host__ __device__ constexpr int header_bytes() {
 
 // Per-warp state of the zero-y grid barrier: REDs into y may only start once every
 // CTA has zeroed its slice of y (see ecsr_tiled_kernel).
+// The CTA's arrival (producer warp, lane 1) publishes target + 1 in shared memory
+// (`target_smem`, 0 = not yet); consumers read it lazily at their first red.
 struct YGate {
     const unsigned long long* counter;
-    unsigned long long target;
+    const unsigned long long* target_smem;
     bool open;
     __device__ __forceinline__ void pass(int lane) {
         if (open) return;
         if (lane == 0) {
+            unsigned long long tgt;
+            do {
+                asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(tgt) : "r"(smem_addr(target_smem)) : "memory");
+            } while (tgt == 0);
+            --tgt;
             unsigned long long v;
             do {
                 asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
-            } while (static_cast<long long>(v - target) < 0);
+            } while (static_cast<long long>(v - tgt) < 0);
         }
         __syncwarp();
         open = true;
@@ -440,9 +448,13 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
     __shared__ unsigned long long gate_target;
     __shared__ uint32_t rec_next;                   // dynamic record scheduler
     __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per ring stage
-    // tile (relative to t0) the producer last put in each stage: a warp may be handed a
-    // record several ring cycles ahead, and an mbarrier parity wait alone would alias
+    // The stages form a pool, not an in-order ring: the producer refills whichever stage
+    // was released (a long record then holds one stage, not the whole ring). It tags a
+    // stage with (tile << 1 | parity of this fill of its full barrier) before the copy;
+    // consumers look their tile up by tag and wait on that parity.
     __shared__ uint32_t stage_tile[kMaxRingStages];
+    __shared__ uint32_t tile_rec_s[kTileRecCache];
+    __shared__ uint32_t stage_free[kMaxRingStages];  // 1: the producer may refill this stage
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -454,12 +466,13 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.nstages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);  // the last finisher of a tile's records arrives
             stage_done[s] = 0;
             stage_tile[s] = 0xffffffffu;
+            stage_free[s] = 1;
         }
         mbar_init(xbar, 1);
         rec_next = 0;
+        gate_target = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -467,28 +480,61 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
 
     if (warp == kProducerWarp) {
         if (!p.zero_y) pdl_trigger();
+        if (p.zero_y && lane > 0) {
+            // Overwrite mode without a memset launch: lanes 1..31 zero this CTA's slice of
+            // y once the predecessor is done (y may alias its inputs), then lane 1 bumps the
+            // generation counter (release: covers the slice via the warp barrier) and
+            // publishes the generation's target; dependents are released only after it.
+            pdl_wait();
+            const int64_t r0 = p.M * blockIdx.x / gridDim.x, r1 = p.M * (blockIdx.x + 1) / gridDim.x;
+            for (int64_t r = r0 + lane - 1; r < r1; r += 31) p.y[r] = 0.0f;
+            __syncwarp(0xfffffffeu);
+            if (lane == 1) {
+                unsigned long long old;
+                asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.sync) : "memory");
+                const unsigned long long tgt = old - old % gridDim.x + gridDim.x;
+                asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_addr(&gate_target)), "l"(tgt + 1)
+                             : "memory");
+                pdl_trigger();
+            }
+        }
         if (lane == 0) {
             const uint64_t policy = l2_evict_first_policy();
-            int stage = 0;
-            uint32_t phase = 0;
+            uint32_t fill_parity = 0;  // bit s: parity of the next fill of stage s
             uint32_t t = t0;
+            int scan = 0;
             // One tile goes out before x: it never depends on the predecessor kernel.
             // The rest waits until x has landed, so the x request is not queued behind
             // this SM's whole weight stream in the memory system.
             auto issue = [&]() {
-                mbar_wait(&empty[stage], phase ^ 1u);
+                int stage = -1;
+                while (stage < 0) {  // any released stage
+                    for (int k = 0; k < p.nstages; ++k) {
+                        const int s2 = (scan + k) % p.nstages;
+                        uint32_t f;
+                        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(f) : "r"(smem_addr(&stage_free[s2])) : "memory");
+                        if (f) {
+                            stage = s2;
+                            break;
+                        }
+                    }
+                    if (stage < 0) __nanosleep(32);
+                }
+                scan = (stage + 1) % p.nstages;
+                stage_free[stage] = 0;
+                // generic-proxy reads of the old tile are complete (their values were
+                // consumed); order them before the async-proxy overwrite
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t par = (fill_parity >> stage) & 1u;
+                fill_parity ^= 1u << stage;
                 const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
                 const uint32_t bytes = (b - a) * 16u;
                 asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_tile[stage])),
-                             "r"(t - t0)
+                             "r"(((t - t0) << 1) | par)
                              : "memory");
                 mbar_arrive_expect_tx(&full[stage], bytes);
                 bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a) * 16u,
                          bytes, &full[stage], policy);
-                if (++stage == p.nstages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
                 ++t;
             };
             if (t < t1) issue();
@@ -510,28 +556,13 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
     ECSR_TRACE(1, threadIdx.x == 0);
     const int tid = threadIdx.x;
     constexpr int nthr = kNumConsumerWarps * 32;
-    if (p.zero_y) {
-        const int64_t r0 = p.M * blockIdx.x / gridDim.x, r1 = p.M * (blockIdx.x + 1) / gridDim.x;
-        for (int64_t r = r0 + tid; r < r1; r += nthr) p.y[r] = 0.0f;
-        __threadfence();
-    }
+
     if (!x_bulk) {
         for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
         consumer_bar_sync();
         if (tid == 0) mbar_arrive(xbar);
     }
-    YGate gate{p.sync, 0ull, !p.zero_y};
-    if (p.zero_y) {
-        consumer_bar_sync();
-        if (tid == 0) {
-            unsigned long long old;
-            asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.sync) : "memory");
-            gate_target = old - old % gridDim.x + gridDim.x;
-        }
-        consumer_bar_sync();
-        gate.target = gate_target;
-        pdl_trigger();
-    }
+    YGate gate{p.sync, &gate_target, !p.zero_y};
     mbar_wait(xbar, 0);
     ECSR_TRACE(2, threadIdx.x == 0);
 
@@ -542,8 +573,16 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
     // records releases its ring stage to the producer.
     const uint32_t rec0 = p.tile_rec[t0];
     const uint32_t nrec_cta = p.tile_rec[t1] - rec0;
+    // record prefix counts of this CTA's tiles, cached in shared memory
+    const uint32_t ntl = t1 - t0;
+    for (uint32_t i = threadIdx.x; i <= ntl && i < kTileRecCache; i += kNumConsumerWarps * 32)
+        tile_rec_s[i] = p.tile_rec[t0 + i] - rec0;
+    consumer_bar_sync();
+    auto tile_rec_at = [&](uint32_t i) -> uint32_t {
+        return i < kTileRecCache ? tile_rec_s[i] : p.tile_rec[t0 + i] - rec0;
+    };
     uint32_t ti = 0;                       // tile cursor (relative to t0)
-    uint32_t tile_end = p.tile_rec[t0 + 1] - rec0;
+    uint32_t tile_end = tile_rec_at(1);
     uint32_t tile_begin = 0;
 #ifdef ECSR_TRACE_CYCLES
     unsigned long long cyc_wait = 0, cyc_work = 0, nwork = 0;
@@ -556,19 +595,25 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
         while (k >= tile_end) {
             ++ti;
             tile_begin = tile_end;
-            tile_end = p.tile_rec[t0 + ti + 1] - rec0;
+            tile_end = tile_rec_at(ti + 1);
         }
-        const uint32_t stage = ti % p.nstages;
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c0 = clock64();
 #endif
-        {  // wait until the producer has put tile ti in this stage, then for its bytes
-            uint32_t cur;
-            do {
-                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(cur) : "r"(smem_addr(&stage_tile[stage])) : "memory");
-            } while (cur != ti);
+        uint32_t stage, par;
+        while (true) {  // find the stage holding tile ti (lane s reads stage s's tag)
+            uint32_t tag = 0xffffffffu;
+            if (lane < p.nstages)
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(smem_addr(&stage_tile[lane])) : "memory");
+            const uint32_t hit = __ballot_sync(0xffffffffu, (tag >> 1) == ti);
+            if (hit) {
+                stage = __ffs(hit) - 1;
+                par = __shfl_sync(0xffffffffu, tag, stage) & 1u;
+                break;
+            }
+            __nanosleep(64);
         }
-        mbar_wait(&full[stage], (ti / p.nstages) & 1u);
+        mbar_wait(&full[stage], par);
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c1 = clock64();
         cyc_wait += c1 - c0;
@@ -590,7 +635,8 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
             const uint32_t done = atomicAdd(&stage_done[stage], 1u) + 1u;
             if (done == th[0]) {  // all records of this tile finished: release the stage
                 stage_done[stage] = 0;
-                mbar_arrive(&empty[stage]);
+                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_free[stage])), "r"(1u)
+                             : "memory");
             }
         }
     }
