@@ -479,17 +479,61 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
     ECSR_TRACE(0, threadIdx.x == 0);
 
     if (warp == kProducerWarp) {
+        // The whole warp runs the producer loop: lanes < nstages poll the stage pool in
+        // parallel (ballot), lane 0 issues the copies. One tile goes out before x: it
+        // never depends on the predecessor kernel; the rest waits until x has landed,
+        // so the x request is not queued behind this SM's whole weight stream.
         if (!p.zero_y) pdl_trigger();
-        if (p.zero_y && lane > 0) {
-            // Overwrite mode without a memset launch: lanes 1..31 zero this CTA's slice of
-            // y once the predecessor is done (y may alias its inputs), then lane 1 bumps the
-            // generation counter (release: covers the slice via the warp barrier) and
-            // publishes the generation's target; dependents are released only after it.
-            pdl_wait();
+        const uint64_t policy = l2_evict_first_policy();
+        uint32_t fill_parity = 0;  // bit s: parity of the next fill of stage s
+        uint32_t t = t0;
+        auto issue = [&]() {
+            uint32_t freeset;
+            while (true) {
+                uint32_t f = 0;
+                if (lane < p.nstages)
+                    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(f) : "r"(smem_addr(&stage_free[lane])) : "memory");
+                freeset = __ballot_sync(0xffffffffu, f != 0);
+                if (freeset) break;
+                __nanosleep(20);
+            }
+            const int stage = __ffs(freeset) - 1;
+            if (lane == 0) {
+                stage_free[stage] = 0;
+                // generic-proxy reads of the old tile are complete (their values were
+                // consumed); order them before the async-proxy overwrite
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t par = (fill_parity >> stage) & 1u;
+                const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
+                const uint32_t bytes = (b - a) * 16u;
+                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_tile[stage])),
+                             "r"(((t - t0) << 1) | par)
+                             : "memory");
+                mbar_arrive_expect_tx(&full[stage], bytes);
+                bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a) * 16u, bytes,
+                         &full[stage], policy);
+            }
+            fill_parity ^= 1u << stage;
+            ++t;
+            __syncwarp();
+        };
+        if (t < t1) issue();
+        if (x_bulk || p.zero_y) pdl_wait();
+        if (x_bulk && lane == 0) {
+            const uint32_t xbytes = static_cast<uint32_t>(p.K) * 2u;
+            mbar_arrive_expect_tx(xbar, xbytes);
+            bulk_g2s(xs, p.x, xbytes, xbar, l2_evict_last_policy());
+        }
+        if (p.zero_y) {
+            // Overwrite mode without a memset launch: zero this CTA's slice of y (after
+            // the predecessor: y may alias its inputs), then bump the generation counter
+            // (release; covers the slice via the warp barrier) and publish the target in
+            // shared memory; PDL dependents are released only after the arrival. The
+            // atomic's latency overlaps the wait for x.
             const int64_t r0 = p.M * blockIdx.x / gridDim.x, r1 = p.M * (blockIdx.x + 1) / gridDim.x;
-            for (int64_t r = r0 + lane - 1; r < r1; r += 31) p.y[r] = 0.0f;
-            __syncwarp(0xfffffffeu);
-            if (lane == 1) {
+            for (int64_t r = r0 + lane; r < r1; r += 32) p.y[r] = 0.0f;
+            __syncwarp();
+            if (lane == 0) {
                 unsigned long long old;
                 asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.sync) : "memory");
                 const unsigned long long tgt = old - old % gridDim.x + gridDim.x;
@@ -497,63 +541,18 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
                              : "memory");
                 pdl_trigger();
             }
+            __syncwarp();
         }
-        if (lane == 0) {
-            const uint64_t policy = l2_evict_first_policy();
-            uint32_t fill_parity = 0;  // bit s: parity of the next fill of stage s
-            uint32_t t = t0;
-            int scan = 0;
-            // One tile goes out before x: it never depends on the predecessor kernel.
-            // The rest waits until x has landed, so the x request is not queued behind
-            // this SM's whole weight stream in the memory system.
-            auto issue = [&]() {
-                int stage = -1;
-                while (stage < 0) {  // any released stage
-                    for (int k = 0; k < p.nstages; ++k) {
-                        const int s2 = (scan + k) % p.nstages;
-                        uint32_t f;
-                        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(f) : "r"(smem_addr(&stage_free[s2])) : "memory");
-                        if (f) {
-                            stage = s2;
-                            break;
-                        }
-                    }
-                    if (stage < 0) __nanosleep(32);
-                }
-                scan = (stage + 1) % p.nstages;
-                stage_free[stage] = 0;
-                // generic-proxy reads of the old tile are complete (their values were
-                // consumed); order them before the async-proxy overwrite
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint32_t par = (fill_parity >> stage) & 1u;
-                fill_parity ^= 1u << stage;
-                const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
-                const uint32_t bytes = (b - a) * 16u;
-                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_tile[stage])),
-                             "r"(((t - t0) << 1) | par)
-                             : "memory");
-                mbar_arrive_expect_tx(&full[stage], bytes);
-                bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a) * 16u,
-                         bytes, &full[stage], policy);
-                ++t;
-            };
-            if (t < t1) issue();
-            if (x_bulk) {
-                pdl_wait();
-                const uint32_t xbytes = static_cast<uint32_t>(p.K) * 2u;
-                mbar_arrive_expect_tx(xbar, xbytes);
-                bulk_g2s(xs, p.x, xbytes, xbar, l2_evict_last_policy());
-            }
-            mbar_wait(xbar, 0);
-            while (t < t1) issue();
-            ECSR_TRACE(5, true);
-        }
+        mbar_wait(xbar, 0);
+        while (t < t1) issue();
+        ECSR_TRACE(5, lane == 0);
         return;
     }
 
     // Consumers: wait for the predecessor (x producer; y may alias its inputs).
     pdl_wait();
     ECSR_TRACE(1, threadIdx.x == 0);
+
     const int tid = threadIdx.x;
     constexpr int nthr = kNumConsumerWarps * 32;
 
