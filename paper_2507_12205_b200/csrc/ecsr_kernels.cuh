@@ -256,16 +256,39 @@ __device__ __forceinline__ void load_deltas(uint32_t addr, uint32_t (&d)[(V + 3)
 // One chunk of one block on one lane: V columns, G rows each. Lane t's running column
 // index advances by its deltas exactly like _speedups.pyx:112-119; products go into
 // the block's G accumulators in the reference order.
+// x byte addresses of a lane's columns in one chunk: column j sits at
+// xa + 2 * (d_0 + ... + d_j). One IDP.4A per column (dot product of the delta bytes
+// with 2 * [1, .., 1, 0, ..]) replaces a byte extract + add, and the V addresses no
+// longer form a dependency chain.
+template <int V>
+__device__ __forceinline__ void chunk_addrs(const uint32_t (&d)[(V + 3) / 4], uint32_t& xa,
+                                            uint32_t (&a)[V]) {
+    constexpr uint32_t kSel[4] = {0x02u, 0x0202u, 0x020202u, 0x02020202u};
+#pragma unroll
+    for (int w = 0; w < (V + 3) / 4; ++w) {
+#pragma unroll
+        for (int j = 0; j < 4 && 4 * w + j < V; ++j) a[4 * w + j] = __dp4a(d[w], kSel[j], xa);
+        xa = a[(4 * w + 3 < V) ? 4 * w + 3 : V - 1];
+    }
+}
+
+#ifdef ECSR_EXP_NOGATHER
+__device__ uint32_t g_xs_dbg;
+#endif
 template <int G, int V, int NW>
 __device__ __forceinline__ void chunk_fma(const uint32_t (&d)[(V + 3) / 4], const uint32_t (&w)[NW],
                                           uint32_t& xa, float* acc) {
+#ifdef ECSR_EXP_NOGATHER
+    const uint32_t xs_dbg = 0;  // shared window offset 0: the barrier area (benign reads)
+#endif
+    uint32_t a[V];
+    chunk_addrs<V>(d, xa, a);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-        xa += 2u * __byte_perm(d[j >> 2], 0u, 0x4440u + (j & 3));
 #ifdef ECSR_EXP_NOGATHER
-        const unsigned short xh = lds_h((xa & 0xfffu) | 0x100u);
+        const unsigned short xh = lds_h(xs_dbg + ((a[j] >> 31) << 1));  // broadcast
 #else
-        const unsigned short xh = lds_h(xa);
+        const unsigned short xh = lds_h(a[j]);
 #endif
 #pragma unroll
         for (int k = 0; k < G; ++k) acc[k] = fhfma(half_at(w, j * G + k), xh, acc[k]);
@@ -386,12 +409,12 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
         uint32_t ptr = body;
 #pragma unroll 1
         for (uint32_t c = 0; c < nch; ++c, ptr += DCH + vch) {
-            uint32_t d[(V + 3) / 4];
+            uint32_t d[(V + 3) / 4], xaddr[V];
             load_deltas<V>(ptr + lane * V, d);
+            chunk_addrs<V>(d, xa, xaddr);
 #pragma unroll
             for (int j = 0; j < V; ++j) {
-                xa += 2u * __byte_perm(d[j >> 2], 0u, 0x4440u + (j & 3));
-                const unsigned short xh = lds_h(xa);
+                const unsigned short xh = lds_h(xaddr[j]);
                 uint32_t w[4];
                 lds_bytes<16>(ptr + DCH + (lane * V + j) * 2u * g + 16u * pass, w);
 #pragma unroll
