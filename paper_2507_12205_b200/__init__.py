@@ -13,6 +13,7 @@ Public API (names follow the reference `ecsr` package, pkg/src/ecsr/__init__.py)
 from .container import (  # noqa: F401
     EcCsrMatrix,
     EcCsrSet,
+    decode_ec_csr,
     deserialize,
     from_reference,
     kernel_model_bytes,

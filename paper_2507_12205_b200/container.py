@@ -321,3 +321,54 @@ def from_reference(ec) -> EcCsrMatrix:
                      np.asarray(s.pad_mask), np.asarray(s.block_values)) for s in ec.sets]
     return EcCsrMatrix(ec.num_rows, ec.num_cols, ec.value_bits, ec.delta_bits,
                        ec.warp_size, sets)
+
+
+# --- decode (storage.py:260-309) ---------------------------------------------
+
+
+def decode_ec_csr(ec):
+    """Scatter every stored entry back into CSR, dropping padding and gap-bridging
+    columns (`pad_mask`), exactly like `storage.decode_ec_csr` (`storage.py:260-309`):
+    the round trip `decode_ec_csr(convert_csr(A)) == A` holds bit for bit."""
+    from .generators import CsrMatrix
+
+    warp = ec.warp_size
+    rows_l, cols_l, vals_l = [], [], []
+    for s in ec.sets:
+        check_set_shapes(s, warp)
+        g, v = s.granularity, s.vector_size
+        for b in range(s.num_blocks):
+            st, en = int(s.block_indptr[b]), int(s.block_indptr[b + 1])
+            n = en - st
+            if n == 0:
+                continue
+            ch = n // (warp * v)
+            d = np.asarray(s.delta_indices[st:en]).reshape(ch, warp, v).transpose(1, 0, 2)
+            d = d.reshape(warp, -1).astype(np.int64)
+            cols = (np.asarray(s.base_indices[b * warp:(b + 1) * warp], np.int64)[:, None]
+                    + np.cumsum(d, axis=1)).reshape(-1)
+            if cols.size and int(cols.max()) >= ec.num_cols:
+                raise ContainerError(f"decoded column {int(cols.max())} out of range {ec.num_cols}")
+            vals = np.asarray(s.block_values[st * g:en * g]).reshape(ch, warp, v * g)
+            vals = vals.transpose(1, 0, 2).reshape(n, g)
+            mask = np.asarray(s.pad_mask[st:en]).reshape(ch, warp, v).transpose(1, 0, 2).reshape(-1)
+            keep = ~mask
+            block_rows = np.asarray(s.row_indices[b * g:(b + 1) * g], np.int64)
+            kc = cols[keep]
+            rows_l.append(np.repeat(block_rows[None, :], kc.size, axis=0).reshape(-1))
+            cols_l.append(np.repeat(kc, g))
+            vals_l.append(vals[keep].reshape(-1))
+    if rows_l:
+        rows, cols, vals = np.concatenate(rows_l), np.concatenate(cols_l), np.concatenate(vals_l)
+    else:
+        rows = cols = np.empty(0, np.int64)
+        vals = np.empty(0, ec.dtype)
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    if rows.size > 1 and np.any((np.diff(rows) == 0) & (np.diff(cols) == 0)):
+        raise ContainerError("duplicate entries while decoding; container is inconsistent")
+    if rows.size and (int(rows.max()) >= ec.num_rows or int(rows.min()) < 0):
+        raise ContainerError("row index out of range while decoding")
+    row_ptr = np.zeros(ec.num_rows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=ec.num_rows), out=row_ptr[1:])
+    return CsrMatrix(ec.num_rows, ec.num_cols, row_ptr, cols, vals)

@@ -267,7 +267,12 @@ int query_limits(int device, DeviceLimits* lim) {
 // ---------------------------------------------------------------------------------
 struct GroupPlan {
     std::vector<std::pair<int, int64_t>> blocks;  // (set, block), container order
+    int P = 1;                                    // block slots of the record (>= blocks)
 };
+
+// A record of P blocks must fit a ring stage next to x: runs of very wide blocks
+// (large K) get fewer blocks per record.
+constexpr int64_t kRecordCap = 24 * 1024;
 
 int group_p(int g) { return g > 8 ? 1 : ecsr::group_blocks(g); }
 
@@ -277,7 +282,7 @@ int64_t block_chunks(const ecsr_host_set& s, int64_t b) {
 
 int64_t group_record_bytes(const ecsr_host_set* sets, const GroupPlan& gp, bool wide) {
     const ecsr_host_set& s0 = sets[gp.blocks[0].first];
-    const int g = s0.granularity, v = s0.vector_size, P = group_p(g);
+    const int g = s0.granularity, v = s0.vector_size, P = gp.P;
     int64_t nmin = INT64_MAX, total = 0;
     for (auto& sb : gp.blocks) {
         const int64_t n = block_chunks(sets[sb.first], sb.second);
@@ -306,7 +311,7 @@ double group_record_cost(const ecsr_host_set* sets, const GroupPlan& gp, bool wi
 void write_group_record(const ecsr_host_set* sets, const std::vector<SetDesc>& desc, const GroupPlan& gp,
                         int host_dtype, bool wide, uint8_t* r) {
     const ecsr_host_set& s0 = sets[gp.blocks[0].first];
-    const int g = s0.granularity, v = s0.vector_size, P = group_p(g);
+    const int g = s0.granularity, v = s0.vector_size, P = gp.P;
     const int nb = static_cast<int>(gp.blocks.size());
     std::vector<int64_t> nch(nb), st(nb);
     int64_t nmin = INT64_MAX;
@@ -330,6 +335,7 @@ void write_group_record(const ecsr_host_set* sets, const std::vector<SetDesc>& d
     r[51] = static_cast<uint8_t>(v);
     r[52] = static_cast<uint8_t>(nb);
     r[53] = present;
+    r[54] = static_cast<uint8_t>(P);
     for (int b = 0; b < nb; ++b)
         std::memcpy(r + 64 + 4 * g * b, sets[gp.blocks[b].first].row_indices + gp.blocks[b].second * g, 4 * g);
     uint8_t* q = r + ecsr::group_header_bytes(g, P);
@@ -384,19 +390,35 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
     tile_rec_start->assign(1, 0u);
     tile_cost->clear();
     *max_tile = 0;
-    // 1. plan records: P consecutive blocks of a (g, v) run
+    // 1. plan records: P consecutive blocks of a (g, v) run; P halves while the run's
+    //    widest block would make a record exceed kRecordCap
     std::vector<std::vector<GroupPlan>> runs;
-    for (int si = 0; si < nsets; ++si) {
-        const ecsr_host_set& s = sets[si];
-        const bool new_run = si == 0 || sets[si - 1].granularity != s.granularity ||
-                             sets[si - 1].vector_size != s.vector_size;
-        if (new_run) runs.emplace_back();
-        const int P = group_p(s.granularity);
-        for (int64_t b = 0; b < s.num_blocks; ++b) {
-            auto& run = runs.back();
-            if (run.empty() || static_cast<int>(run.back().blocks.size()) == P) run.emplace_back();
-            run.back().blocks.emplace_back(si, b);
-        }
+    std::vector<int> run_p;
+    for (int si = 0; si < nsets;) {
+        int se = si + 1;
+        while (se < nsets && sets[se].granularity == sets[si].granularity &&
+               sets[se].vector_size == sets[si].vector_size)
+            ++se;
+        const int g = sets[si].granularity, v = sets[si].vector_size;
+        int64_t widest = 0;
+        for (int k = si; k < se; ++k)
+            for (int64_t b = 0; b < sets[k].num_blocks; ++b) widest = std::max(widest, block_chunks(sets[k], b));
+        const int64_t chunk = 32 * v + 64 * v * g;
+        int P = group_p(g);
+        while (v == 4 && P > 1 &&  // the kernel has reduced-P variants for v = 4 only
+               ecsr::group_header_bytes(g, P) + (wide ? 128 : 64) * P + P * widest * chunk > kRecordCap)
+            P /= 2;
+        runs.emplace_back();
+        for (int k = si; k < se; ++k)
+            for (int64_t b = 0; b < sets[k].num_blocks; ++b) {
+                auto& run = runs.back();
+                if (run.empty() || static_cast<int>(run.back().blocks.size()) == P) {
+                    run.emplace_back();
+                    run.back().P = P;
+                }
+                run.back().blocks.emplace_back(k, b);
+            }
+        si = se;
     }
     // 2. pack records into tiles of <= tile_target() bytes
     auto hdr_of = [](size_t n) { return round_up(8 + 2 * static_cast<int64_t>(n), 16); };
@@ -420,6 +442,8 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
             const ecsr_host_set& s0 = sets[run[i].blocks[0].first];
             const uint16_t gv = static_cast<uint16_t>((s0.granularity << 8) | s0.vector_size);
             std::memcpy(base + 4, &gv, 2);
+            const uint16_t p16 = static_cast<uint16_t>(run[i].P);
+            std::memcpy(base + 6, &p16, 2);
             int64_t off = hdr;
             double cost = 0;
             for (size_t k = 0; k < n; ++k) {
@@ -916,7 +940,7 @@ int ecsr_b200_unpack(const ecsr_dev* d, ecsr_out_set* out, int32_t nsets, int32_
                 const uint8_t* r = tile + 16 * off16;
                 uint16_t nmin;
                 std::memcpy(&nmin, r + 48, 2);
-                const int g = r[50], v = r[51], nb = r[52], P = group_p(g);
+                const int g = r[50], v = r[51], nb = r[52], P = r[54];
                 const int esz = d->wide ? 4 : 2;
                 const uint8_t* q = r + ecsr::group_header_bytes(g, P);
                 const uint8_t* body = q + 32 * P * esz;

@@ -314,10 +314,9 @@ __device__ __forceinline__ void emit_row(uint32_t r, int g, int P, int blk, int 
 // accumulates its segment sequentially (reference order); the 8 accumulators then
 // share one butterfly reduce-scatter whose per-accumulator association is the
 // reference's lane tree (_speedups.pyx:120-127).
-template <int G, int V>
+template <int G, int V, int P>
 __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const TiledParams& p,
                                                    YGate& gate) {
-    constexpr int P = group_blocks(G);
     constexpr int NACC = P * G;
     uint32_t m[2];
     lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
@@ -427,25 +426,30 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
     }
 }
 
-__device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t xs, int lane,
+__device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P, uint32_t xs, int lane,
                                              const TiledParams& p, YGate& gate) {
     const int g = static_cast<int>(gv >> 8);
     const bool v4 = (gv & 0xffu) == 4;
-    if (g == 1) {
-        if (v4) tiled_group_record<1, 4>(r, xs, lane, p, gate);
-        else tiled_group_record<1, 1>(r, xs, lane, p, gate);
-    } else if (g == 2) {
-        if (v4) tiled_group_record<2, 4>(r, xs, lane, p, gate);
-        else tiled_group_record<2, 1>(r, xs, lane, p, gate);
-    } else if (g == 4) {
-        if (v4) tiled_group_record<4, 4>(r, xs, lane, p, gate);
-        else tiled_group_record<4, 1>(r, xs, lane, p, gate);
-    } else if (g == 8) {
-        if (v4) tiled_group_record<8, 4>(r, xs, lane, p, gate);
-        else tiled_group_record<8, 1>(r, xs, lane, p, gate);
-    } else {  // 16, 32: passes of 8 rows
-        if (v4) tiled_wide_record<4>(r, g, xs, lane, p, gate);
+    if (!v4) {  // short 1-grained sets (v = 1, storage.py:99-122) and other narrow blocks
+        if (g == 1) tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate);
+        else if (g == 2) tiled_group_record<2, 1, group_blocks(2)>(r, xs, lane, p, gate);
+        else if (g == 4) tiled_group_record<4, 1, group_blocks(4)>(r, xs, lane, p, gate);
+        else if (g == 8) tiled_group_record<8, 1, 1>(r, xs, lane, p, gate);
         else tiled_wide_record<1>(r, g, xs, lane, p, gate);
+        return;
+    }
+    switch ((g << 4) | P) {  // (g, blocks per record) of this run (packer: kRecordCap)
+        case (1 << 4) | 8: tiled_group_record<1, 4, 8>(r, xs, lane, p, gate); break;
+        case (1 << 4) | 4: tiled_group_record<1, 4, 4>(r, xs, lane, p, gate); break;
+        case (1 << 4) | 2: tiled_group_record<1, 4, 2>(r, xs, lane, p, gate); break;
+        case (1 << 4) | 1: tiled_group_record<1, 4, 1>(r, xs, lane, p, gate); break;
+        case (2 << 4) | 4: tiled_group_record<2, 4, 4>(r, xs, lane, p, gate); break;
+        case (2 << 4) | 2: tiled_group_record<2, 4, 2>(r, xs, lane, p, gate); break;
+        case (2 << 4) | 1: tiled_group_record<2, 4, 1>(r, xs, lane, p, gate); break;
+        case (4 << 4) | 2: tiled_group_record<4, 4, 2>(r, xs, lane, p, gate); break;
+        case (4 << 4) | 1: tiled_group_record<4, 4, 1>(r, xs, lane, p, gate); break;
+        case (8 << 4) | 1: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate); break;
+        default: tiled_wide_record<4>(r, g, xs, lane, p, gate); break;  // g = 16, 32
     }
 }
 
@@ -647,7 +651,7 @@ __global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __gr
         const uint32_t gv = th[1] & 0xffffu;
         uint32_t off16;
         lds_bytes<2>(tile + 8 + 2 * (k - tile_begin), &off16);
-        if (!(p.debug & 1)) tiled_record(tile + 16u * off16, gv, xs_addr, lane, p, gate);
+        if (!(p.debug & 1)) tiled_record(tile + 16u * off16, gv, th[1] >> 16, xs_addr, lane, p, gate);
 #ifdef ECSR_TRACE_CYCLES
         cyc_work += clock64() - c1;
         ++nwork;

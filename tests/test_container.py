@@ -112,3 +112,22 @@ def test_planted_blocks_has_shared_patterns():
         pats[key] = pats.get(key, 0) + 1
     sizes = sorted(pats.values(), reverse=True)
     assert sizes[0] == 8 and 4 in sizes and 2 in sizes
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_decode_round_trip_and_matches_reference_decode(name):
+    # storage.decode_ec_csr (storage.py:260-309): decode(convert(A)) == A exactly
+    import sys
+
+    from conftest import GOLDEN
+
+    sys.path.insert(0, GOLDEN)
+    from cases import golden_matrix
+
+    g = load_golden(name)
+    case = golden_manifest()[name]
+    a = golden_matrix(case)
+    d = C.decode_ec_csr(g["ec"])
+    assert np.array_equal(d.row_ptr, a.row_ptr)
+    assert np.array_equal(d.col_idx, a.col_idx)
+    assert np.array_equal(d.values, np.asarray(a.values, dtype=d.values.dtype))
