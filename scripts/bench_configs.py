@@ -1,0 +1,128 @@
+"""Per-config SpMV measurements for BASELINE.json configs 1-5 (writes one JSON line each).
+
+    python scripts/bench_configs.py [--out profiles/round1/configs.jsonl] [--only 1,3]
+
+Inputs: seeded synthetic matrices (magnitude-pruned N(0, 1/K) or planted blocks),
+encoded by the native encoder (byte-identical to the reference convert_csr). For each
+matrix: `stream_us` = average device time per SpMV when launched back to back (CUDA
+graph over rotating copies whose total exceeds 2x L2, as in a layer sequence),
+`single_us` = one launch after a 256 MB L2 flush, GB/s = model bytes / time, frac vs
+the 6.65 TB/s fallback HBM peak. Parity: fast-mode y vs the C oracle on fp16-rounded
+inputs (rel-inf). Config 5 reports the per-GPU shard SpMV of an N-way row split
+(the NCCL all-gather needs more than the one GPU available here).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_2507_12205_b200.container import kernel_model_bytes  # noqa: E402
+from paper_2507_12205_b200.device import spmv, to_device  # noqa: E402
+from paper_2507_12205_b200.encoder import convert_csr  # noqa: E402
+from paper_2507_12205_b200.generators import make_matrix  # noqa: E402
+from paper_2507_12205_b200.sharded import row_slice, shard_bounds  # noqa: E402
+
+PEAK = 6650.0
+L2 = 126 << 20
+
+CONFIGS = {
+    1: [("4096x4096@50%", "magnitude", 4096, 4096, 0.5, 1, None)],
+    2: [(f"{n}@{int(s * 100)}%", "magnitude", m, k, s, 200 + i, None)
+        for s in (0.5, 0.6, 0.7)
+        for i, (n, m, k) in enumerate((("q 4096x4096", 4096, 4096), ("up 11008x4096", 11008, 4096),
+                                       ("down 4096x11008", 4096, 11008)))],
+    3: [("13B-q 5120x5120 planted@50%", "planted", 5120, 5120, 0.5, 301, None),
+        ("13B-up 13824x5120 planted@50%", "planted", 13824, 5120, 0.5, 302, None),
+        ("13B-q 5120x5120 planted@70%", "planted", 5120, 5120, 0.7, 303, None)],
+    4: [("OPT30B-q 7168x7168@70%", "magnitude", 7168, 7168, 0.7, 401, None),
+        ("OPT30B-fc1 28672x7168@70%", "magnitude", 28672, 7168, 0.7, 402, None),
+        ("OPT30B-fc2 7168x28672@70%", "magnitude", 7168, 28672, 0.7, 403, None)],
+    5: [(f"70B-{n} shard 0/{p}", "magnitude", m, 8192, 0.5, 500 + j, p)
+        for j, (n, m) in enumerate((("q 8192x8192", 8192), ("up 28672x8192", 28672)))
+        for p in (1, 2, 4, 8)],
+}
+
+
+def time_graph(fn, reps):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / reps
+
+
+def measure(label, kind, m, k, s, seed, shards):
+    t0 = time.time()
+    a = make_matrix(kind, m, k, s, seed, dtype=np.float32)
+    if shards:
+        b = shard_bounds(a.row_ptr, shards)
+        a = row_slice(a, b[0], b[1])
+    ec = convert_csr(a)
+    enc_s = time.time() - t0
+    mb = kernel_model_bytes(ec)
+    ncopy = max(1, int(np.ceil(2.2 * L2 / mb)))
+    Ws = [to_device(ec) for _ in range(ncopy)]
+    x = np.random.default_rng(seed).uniform(-1, 1, k).astype(np.float16)
+    xd = torch.from_numpy(x).cuda()
+    ys = [torch.empty(ec.num_rows, device="cuda") for _ in range(ncopy)]
+    y = spmv(Ws[0], xd, y=ys[0]).cpu().numpy()
+    ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32), x.astype(np.float32), np.float32)
+    rel = float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
+    stream_us = time_graph(lambda: [spmv(Ws[i], xd, y=ys[i]) for i in range(ncopy)], 20) / ncopy
+    flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
+    singles = []
+    for _ in range(10):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        spmv(Ws[0], xd, y=ys[0])
+        e1.record()
+        torch.cuda.synchronize()
+        singles.append(e0.elapsed_time(e1) * 1e3)
+    single_us = float(np.median(singles))
+    return {"matrix": label, "rows": ec.num_rows, "cols": k, "nnz": ec.nnz,
+            "shards": shards, "model_bytes": mb, "layout": Ws[0].layout,
+            "stream_us": round(stream_us, 2), "stream_GBps": round(mb / stream_us / 1e3, 1),
+            "stream_frac": round(mb / stream_us / 1e3 / PEAK, 3),
+            "single_us": round(single_us, 2), "single_GBps": round(mb / single_us / 1e3, 1),
+            "parity_rel_inf": rel, "encode_s": round(enc_s, 1),
+            "sets": [(st.granularity, st.vector_size, st.num_blocks) for st in ec.sets]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.jsonl"))
+    ap.add_argument("--only", default="1,2,3,4,5")
+    args = ap.parse_args()
+    with open(args.out, "w") as fh:
+        for c in [int(v) for v in args.only.split(",")]:
+            for case in CONFIGS[c]:
+                r = measure(*case)
+                r["config"] = c
+                line = json.dumps(r)
+                print(line, flush=True)
+                fh.write(line + "\n")
+                fh.flush()
+
+
+if __name__ == "__main__":
+    main()
