@@ -41,7 +41,7 @@ int fail(int code, const std::string& msg) {
 int tile_target() {  // bytes of whole blocks per tile (balance granularity); env override for tuning
     static int v = [] {
         const char* e = std::getenv("ECSR_B200_TILE");
-        return e ? std::max(1024, std::atoi(e)) : 32768;
+        return e ? std::max(1024, std::atoi(e)) : 16384;
     }();
     return v;
 }
@@ -238,11 +238,13 @@ bool pow2_le32(int g) { return g == 1 || g == 2 || g == 4 || g == 8 || g == 16 |
 struct DeviceLimits {
     int sms = 148;
     int smem_optin = 232448;
+    int smem_per_sm = 233472;
 };
 
 int query_limits(int device, DeviceLimits* lim) {
     ECSR_CUDA(cudaDeviceGetAttribute(&lim->sms, cudaDevAttrMultiProcessorCount, device));
     ECSR_CUDA(cudaDeviceGetAttribute(&lim->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    ECSR_CUDA(cudaDeviceGetAttribute(&lim->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
     return ECSR_OK;
 }
 
@@ -735,7 +737,10 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                           &max_tile);
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
-        const int64_t avail = lim.smem_optin - 3072 - 16 * kMaxStages - xbytes;  // static smem + barriers
+        // shared memory per CTA: kCtasPerSm CTAs share the SM's 228 KB (1 KB reserved each)
+        const int64_t cta_smem = ecsr::kCtasPerSm == 1 ? lim.smem_optin
+                                                      : (lim.smem_per_sm / ecsr::kCtasPerSm) - 1024;
+        const int64_t avail = cta_smem - 3072 - 16 * kMaxStages - xbytes;  // static smem + barriers
         const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
         if (stage > kMaxStageBytes || nst < 2 || arena.size() / 16 >= (1ull << 32)) tiled = false;
         if (tiled) {
@@ -746,7 +751,8 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             d->smem_bytes = static_cast<int>(round_up(16 * nst + 8, 128) + nst * stage + xbytes);
             const int64_t ntiles = static_cast<int64_t>(tstart.size()) - 1;
             d->ntiles = ntiles;
-            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(lim.sms, ntiles)));
+            const int grid =
+                static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t{lim.sms} * ecsr::kCtasPerSm, ntiles)));
             d->grid = grid;
             // cost-balanced contiguous tile ranges (HBM bytes + consumer issue estimate)
             std::vector<uint32_t> cta(grid + 1, 0);

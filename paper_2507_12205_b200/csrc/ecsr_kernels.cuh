@@ -34,9 +34,13 @@
 
 namespace ecsr {
 
-#ifndef ECSR_NCONS
-#define ECSR_NCONS 16
+#ifndef ECSR_CTAS_PER_SM
+#define ECSR_CTAS_PER_SM 2
 #endif
+#ifndef ECSR_NCONS
+#define ECSR_NCONS (16 / ECSR_CTAS_PER_SM)
+#endif
+constexpr int kCtasPerSm = ECSR_CTAS_PER_SM;  // co-resident CTAs (consecutive launches overlap)
 constexpr int kNumConsumerWarps = ECSR_NCONS;
 constexpr int kThreadsTiled = 32 * (kNumConsumerWarps + 1);
 constexpr int kProducerWarp = kNumConsumerWarps;
@@ -465,7 +469,7 @@ __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P
 // generation's multiple of gridDim.x) before their first red.global. PDL dependents
 // are released only after the arrival, so back-to-back launches of one handle never
 // interleave their generations.
-__global__ void __launch_bounds__(kThreadsTiled, 1) ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
+__global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + p.nstages;
