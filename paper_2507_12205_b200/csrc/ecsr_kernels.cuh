@@ -580,18 +580,23 @@ __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(c
         return;
     }
 
-    // Consumers: wait for the predecessor (x producer; y may alias its inputs).
+    // Consumers. The record prefix counts of this CTA's tiles are cached in shared
+    // memory first: they never depend on the previous kernel, so these loads overlap
+    // the wait for the predecessor and for x.
+    const int tid = threadIdx.x;
+    constexpr int nthr = kNumConsumerWarps * 32;
+    const uint32_t rec0 = p.tile_rec[t0];
+    const uint32_t nrec_cta = p.tile_rec[t1] - rec0;
+    const uint32_t ntl = t1 - t0;
+    for (uint32_t i = tid; i <= ntl && i < kTileRecCache; i += nthr) tile_rec_s[i] = p.tile_rec[t0 + i] - rec0;
+    // wait for the predecessor (x producer; y may alias its inputs)
     pdl_wait();
     ECSR_TRACE(1, threadIdx.x == 0);
 
-    const int tid = threadIdx.x;
-    constexpr int nthr = kNumConsumerWarps * 32;
-
-    if (!x_bulk) {
+    if (!x_bulk)
         for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
-        consumer_bar_sync();
-        if (tid == 0) mbar_arrive(xbar);
-    }
+    consumer_bar_sync();  // tile_rec_s (and a consumer-copied x) complete
+    if (!x_bulk && tid == 0) mbar_arrive(xbar);
     YGate gate{p.sync, &gate_target, !p.zero_y};
     mbar_wait(xbar, 0);
     ECSR_TRACE(2, threadIdx.x == 0);
@@ -601,13 +606,6 @@ __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(c
     // Dynamic scheduling: warps take the CTA's records in container order from a
     // shared counter (balances unequal records); the last warp to finish a tile's
     // records releases its ring stage to the producer.
-    const uint32_t rec0 = p.tile_rec[t0];
-    const uint32_t nrec_cta = p.tile_rec[t1] - rec0;
-    // record prefix counts of this CTA's tiles, cached in shared memory
-    const uint32_t ntl = t1 - t0;
-    for (uint32_t i = threadIdx.x; i <= ntl && i < kTileRecCache; i += kNumConsumerWarps * 32)
-        tile_rec_s[i] = p.tile_rec[t0 + i] - rec0;
-    consumer_bar_sync();
     auto tile_rec_at = [&](uint32_t i) -> uint32_t {
         return i < kTileRecCache ? tile_rec_s[i] : p.tile_rec[t0 + i] - rec0;
     };
