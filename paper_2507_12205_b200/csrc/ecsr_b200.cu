@@ -148,6 +148,7 @@ struct ecsr_dev {
     uint32_t* d_cta_tile = nullptr;
     uint32_t* d_tile_rec = nullptr;        // [ntiles + 1] record prefix counts
     unsigned long long* d_sync = nullptr;  // zero-y grid-barrier generation counter
+    bool lean = false;                     // every run uses a lean-kernel record variant
     unsigned long long* d_trace = nullptr; // debug timeline (ECSR_B200_DEBUG & 4)
     int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
     // ordered reduction
@@ -580,7 +581,9 @@ int configure_tiled_kernels(int smem) {
     static int configured = 0;
     std::lock_guard<std::mutex> lock(mu);
     if (configured >= smem) return ECSR_OK;
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
     return ECSR_OK;
@@ -735,6 +738,18 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
         int64_t max_tile = 0;
         build_tiled_arena(sets, nsets, d->sets, host_value_dtype, wide, &arena, &tstart, &trec, &tcost,
                           &max_tile);
+        // the lean kernel covers v = 4 runs with the default blocks-per-record and
+        // g <= 8, and v = 1 runs of g = 1 (the reference's short set)
+        d->lean = true;
+        for (int64_t t = 0; t + 1 < static_cast<int64_t>(tstart.size()); ++t) {
+            const uint8_t* th = arena.data() + 16ull * tstart[t];
+            uint16_t gv, pp;
+            std::memcpy(&gv, th + 4, 2);
+            std::memcpy(&pp, th + 6, 2);
+            const int g = gv >> 8, v = gv & 0xff;
+            const bool ok = (v == 4 && g <= 8 && pp == group_p(g)) || (v == 1 && g == 1);
+            if (!ok) d->lean = false;
+        }
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
         // shared memory per CTA: kCtasPerSm CTAs share the SM's 228 KB (1 KB reserved each)
@@ -863,8 +878,10 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
             p.trace = dm->d_trace;
         }
         p.wide = d->wide;
-        cudaError_t e = launch_pdl(ecsr::ecsr_tiled_kernel, dim3(d->grid), dim3(ecsr::kThreadsTiled),
-                                   d->smem_bytes, st, p);
+        cudaError_t e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false>, dim3(d->grid),
+                                             dim3(ecsr::kThreadsTiled), d->smem_bytes, st, p)
+                                : launch_pdl(ecsr::ecsr_tiled_kernel<true>, dim3(d->grid),
+                                             dim3(ecsr::kThreadsTiled), d->smem_bytes, st, p);
         ECSR_CUDA(e);
         if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
         return ECSR_OK;

@@ -430,10 +430,27 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
     }
 }
 
+// kFull: every (g, v, P) record variant; otherwise only the common ones (v = 4 with
+// the default P, v = 1 with g = 1) -- a smaller kernel body keeps the instruction
+// cache warm; the packer picks the lean kernel when the container needs nothing else.
+template <bool kFull>
 __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P, uint32_t xs, int lane,
                                              const TiledParams& p, YGate& gate) {
     const int g = static_cast<int>(gv >> 8);
     const bool v4 = (gv & 0xffu) == 4;
+    if constexpr (!kFull) {
+        if (!v4) {
+            tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate);
+            return;
+        }
+        switch (g) {
+            case 1: tiled_group_record<1, 4, group_blocks(1)>(r, xs, lane, p, gate); break;
+            case 2: tiled_group_record<2, 4, group_blocks(2)>(r, xs, lane, p, gate); break;
+            case 4: tiled_group_record<4, 4, group_blocks(4)>(r, xs, lane, p, gate); break;
+            default: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate); break;
+        }
+        return;
+    }
     if (!v4) {  // short 1-grained sets (v = 1, storage.py:99-122) and other narrow blocks
         if (g == 1) tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate);
         else if (g == 2) tiled_group_record<2, 1, group_blocks(2)>(r, xs, lane, p, gate);
@@ -469,6 +486,7 @@ __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P
 // generation's multiple of gridDim.x) before their first red.global. PDL dependents
 // are released only after the arrival, so back-to-back launches of one handle never
 // interleave their generations.
+template <bool kFull>
 __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -653,7 +671,7 @@ __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(c
         const uint32_t gv = th[1] & 0xffffu;
         uint32_t off16;
         lds_bytes<2>(tile + 8 + 2 * (k - tile_begin), &off16);
-        if (!(p.debug & 1)) tiled_record(tile + 16u * off16, gv, th[1] >> 16, xs_addr, lane, p, gate);
+        if (!(p.debug & 1)) tiled_record<kFull>(tile + 16u * off16, gv, th[1] >> 16, xs_addr, lane, p, gate);
 #ifdef ECSR_TRACE_CYCLES
         cyc_work += clock64() - c1;
         ++nwork;
