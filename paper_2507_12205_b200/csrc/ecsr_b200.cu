@@ -339,6 +339,9 @@ void write_group_record(const ecsr_host_set* sets, const std::vector<SetDesc>& d
     r[52] = static_cast<uint8_t>(nb);
     r[53] = present;
     r[54] = static_cast<uint8_t>(P);
+    uint8_t has_tail = 0;
+    for (int b = 0; b < nb; ++b) has_tail |= nch[b] > nmin ? 1 : 0;
+    r[55] = has_tail;  // the kernel skips all tail loops at once when no block has one
     for (int b = 0; b < nb; ++b)
         std::memcpy(r + 64 + 4 * g * b, sets[gp.blocks[b].first].row_indices + gp.blocks[b].second * g, 4 * g);
     uint8_t* q = r + ecsr::group_header_bytes(g, P);

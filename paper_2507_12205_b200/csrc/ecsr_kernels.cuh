@@ -326,8 +326,7 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
     lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
     const uint32_t nmin = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
     if (!present) return;  // zero-width blocks only (_speedups.pyx:105-106)
-    uint32_t tl[(P + 1) / 2];
-    lds_bytes<2 * P>(r + 32, tl);  // ntail[P]
+    const bool has_tail = (m[1] >> 24) != 0;  // header byte 55
     const uint32_t q = r + group_header_bytes(G, P);
     uint32_t xa[P];
     if (p.wide) {
@@ -365,15 +364,19 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
 #pragma unroll
         for (int b = 0; b < P; ++b) chunk_fma<G, V, NW>(d[b], w[b], xa[b], acc + b * G);
     }
+    if (has_tail) {  // blocks of a record are near-equal (sorted by nnz): usually none
+        uint32_t tl[(P + 1) / 2];
+        lds_bytes<2 * P>(r + 32, tl);  // ntail[P]
 #pragma unroll
-    for (int b = 0; b < P; ++b) {  // tails: chunks beyond nmin, block after block
-        const uint32_t nt = (tl[b >> 1] >> (16 * (b & 1))) & 0xffffu;
+        for (int b = 0; b < P; ++b) {  // tails: chunks beyond nmin, block after block
+            const uint32_t nt = (tl[b >> 1] >> (16 * (b & 1))) & 0xffffu;
 #pragma unroll 1
-        for (uint32_t c = 0; c < nt; ++c, ptr += DCH + VCH) {
-            uint32_t d[(V + 3) / 4], w[NW];
-            load_deltas<V>(ptr + lane * V, d);
-            lds_bytes<LV>(ptr + DCH + lane * LV, w);
-            chunk_fma<G, V, NW>(d, w, xa[b], acc + b * G);
+            for (uint32_t c = 0; c < nt; ++c, ptr += DCH + VCH) {
+                uint32_t d[(V + 3) / 4], w[NW];
+                load_deltas<V>(ptr + lane * V, d);
+                lds_bytes<LV>(ptr + DCH + lane * LV, w);
+                chunk_fma<G, V, NW>(d, w, xa[b], acc + b * G);
+            }
         }
     }
     const float sum = warp_reduce_scatter<NACC>(acc, lane);
