@@ -45,6 +45,13 @@ int tile_target() {  // bytes of whole blocks per tile (balance granularity); en
     }();
     return v;
 }
+int pre_tiles() {  // tiles streamed before griddepcontrol.wait and the x copy
+    static int v = [] {
+        const char* e = std::getenv("ECSR_B200_PRE");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    return v;
+}
 int debug_flags() {  // tuning experiments only: 1 = consumers skip compute, 2 = no y memset
     static int v = [] {
         const char* e = std::getenv("ECSR_B200_DEBUG");
@@ -864,6 +871,7 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
         p.nstages = d->nstages;
         p.x_vec16 = (reinterpret_cast<uintptr_t>(x) % 16) == 0;
         p.debug = debug_flags();
+        p.pre_tiles = std::min(pre_tiles(), std::max(1, d->nstages - 1));
         p.sync = d->d_sync;
         p.M = d->M;
         p.zero_y = (!ordered && !accumulate) ? 1 : 0;

@@ -65,6 +65,7 @@ struct TiledParams {
     int32_t zero_y;                // overwrite: the kernel zeroes y itself (no memset launch)
     int32_t wide;                  // K > 65535: u32 bases (else u16)
     int32_t debug;                 // tuning experiments (ECSR_B200_DEBUG)
+    int32_t pre_tiles;             // tiles streamed before griddepcontrol.wait / x
     unsigned long long* trace;     // debug timeline [grid][8] (globaltimer ns) or null
 };
 
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(c
             ++t;
             __syncwarp();
         };
-        if (t < t1) issue();
+        for (int k = 0; k < p.pre_tiles && t < t1; ++k) issue();
         if (x_bulk || p.zero_y) pdl_wait();
         if (x_bulk && lane == 0) {
             const uint32_t xbytes = static_cast<uint32_t>(p.K) * 2u;
