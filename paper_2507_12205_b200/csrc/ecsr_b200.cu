@@ -38,12 +38,15 @@ int fail(int code, const std::string& msg) {
             return fail(ECSR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-int tile_target() {  // bytes of whole blocks per tile (balance granularity); env override for tuning
-    static int v = [] {
+// bytes of whole records per tile: 16 KB with two CTAs per SM, 32 KB with one
+// (ECSR_B200_TILE overrides, for tuning)
+int g_tile_default = 16384;
+int tile_target() {
+    static int env = [] {
         const char* e = std::getenv("ECSR_B200_TILE");
-        return e ? std::max(1024, std::atoi(e)) : 16384;
+        return e ? std::max(1024, std::atoi(e)) : 0;
     }();
-    return v;
+    return env ? env : g_tile_default;
 }
 int pre_tiles() {  // tiles streamed before griddepcontrol.wait and the x copy
     static int v = [] {
@@ -156,6 +159,7 @@ struct ecsr_dev {
     uint32_t* d_tile_rec = nullptr;        // [ntiles + 1] record prefix counts
     unsigned long long* d_sync = nullptr;  // zero-y grid-barrier generation counter
     bool lean = false;                     // every run uses a lean-kernel record variant
+    int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
     unsigned long long* d_trace = nullptr; // debug timeline (ECSR_B200_DEBUG & 4)
     int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
     // ordered reduction
@@ -591,9 +595,13 @@ int configure_tiled_kernels(int smem) {
     static int configured = 0;
     std::lock_guard<std::mutex> lock(mu);
     if (configured >= smem) return ECSR_OK;
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true>,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, 8>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false>,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, 8>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, 16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, 16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
     return ECSR_OK;
@@ -741,7 +749,15 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             if ((sets[si].block_indptr[b + 1] - sets[si].block_indptr[b]) / (32 * v) > 65535) tiled = false;
     }
     const bool wide = num_cols > 65535;
+    // Two co-resident CTAs per SM (8 consumer warps each; consecutive launches overlap)
+    // while x is small; one CTA of 16 consumer warps when two copies of x would crowd
+    // out the stage pool.
+    const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
+    const int ctas_per_sm = xbytes <= 32768 ? 2 : 1;
     if (tiled) {
+        static std::mutex tile_mu;  // the packer is host code; serialise the tile default
+        std::lock_guard<std::mutex> lock(tile_mu);
+        g_tile_default = ctas_per_sm == 2 ? 16384 : 32768;
         std::vector<uint8_t> arena;
         std::vector<uint32_t> tstart, trec;
         std::vector<double> tcost;
@@ -761,10 +777,8 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             if (!ok) d->lean = false;
         }
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
-        const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
-        // shared memory per CTA: kCtasPerSm CTAs share the SM's 228 KB (1 KB reserved each)
-        const int64_t cta_smem = ecsr::kCtasPerSm == 1 ? lim.smem_optin
-                                                      : (lim.smem_per_sm / ecsr::kCtasPerSm) - 1024;
+        d->ctas_per_sm = ctas_per_sm;  // CTAs share the SM's 228 KB (1 KB reserved each)
+        const int64_t cta_smem = ctas_per_sm == 1 ? lim.smem_optin : (lim.smem_per_sm / ctas_per_sm) - 1024;
         const int64_t avail = cta_smem - 3072 - 16 * kMaxStages - xbytes;  // static smem + barriers
         const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
         if (stage > kMaxStageBytes || nst < 2 || arena.size() / 16 >= (1ull << 32)) tiled = false;
@@ -777,7 +791,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             const int64_t ntiles = static_cast<int64_t>(tstart.size()) - 1;
             d->ntiles = ntiles;
             const int grid =
-                static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t{lim.sms} * ecsr::kCtasPerSm, ntiles)));
+                static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t{lim.sms} * ctas_per_sm, ntiles)));
             d->grid = grid;
             // cost-balanced contiguous tile ranges (HBM bytes + consumer issue estimate)
             std::vector<uint32_t> cta(grid + 1, 0);
@@ -889,10 +903,15 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
             p.trace = dm->d_trace;
         }
         p.wide = d->wide;
-        cudaError_t e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false>, dim3(d->grid),
-                                             dim3(ecsr::kThreadsTiled), d->smem_bytes, st, p)
-                                : launch_pdl(ecsr::ecsr_tiled_kernel<true>, dim3(d->grid),
-                                             dim3(ecsr::kThreadsTiled), d->smem_bytes, st, p);
+        const int nc = ecsr::kConsumerWarpsPerSm / d->ctas_per_sm;
+        const dim3 blk(ecsr::tiled_threads(nc)), grd(d->grid);
+        cudaError_t e;
+        if (nc == 8)
+            e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false, 8>, grd, blk, d->smem_bytes, st, p)
+                        : launch_pdl(ecsr::ecsr_tiled_kernel<true, 8>, grd, blk, d->smem_bytes, st, p);
+        else
+            e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false, 16>, grd, blk, d->smem_bytes, st, p)
+                        : launch_pdl(ecsr::ecsr_tiled_kernel<true, 16>, grd, blk, d->smem_bytes, st, p);
         ECSR_CUDA(e);
         if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
         return ECSR_OK;

@@ -34,16 +34,10 @@
 
 namespace ecsr {
 
-#ifndef ECSR_CTAS_PER_SM
-#define ECSR_CTAS_PER_SM 2
-#endif
-#ifndef ECSR_NCONS
-#define ECSR_NCONS (16 / ECSR_CTAS_PER_SM)
-#endif
-constexpr int kCtasPerSm = ECSR_CTAS_PER_SM;  // co-resident CTAs (consecutive launches overlap)
-constexpr int kNumConsumerWarps = ECSR_NCONS;
-constexpr int kThreadsTiled = 32 * (kNumConsumerWarps + 1);
-constexpr int kProducerWarp = kNumConsumerWarps;
+// 16 consumer warps per SM: either 2 co-resident CTAs of 8 (consecutive launches
+// overlap; x fits twice) or 1 CTA of 16 (large K: x would not leave room for stages).
+constexpr int kConsumerWarpsPerSm = 16;
+__host__ __device__ constexpr int tiled_threads(int nc) { return 32 * (nc + 1); }
 constexpr int kMaxRingStages = 16;
 constexpr uint32_t kTileRecCache = 256;  // per-CTA record prefix counts kept in smem
 
@@ -133,8 +127,9 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+template <int NC>
 __device__ __forceinline__ void consumer_bar_sync() {
-    asm volatile("bar.sync 1, %0;" ::"r"(kNumConsumerWarps * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
 }
 
 // ---------------------------------------------------------------------------------
@@ -490,8 +485,10 @@ __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P
 // generation's multiple of gridDim.x) before their first red.global. PDL dependents
 // are released only after the arrival, so back-to-back launches of one handle never
 // interleave their generations.
-template <bool kFull>
-__global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
+template <bool kFull, int NC>
+__global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
+    ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
+    constexpr int kProducerWarp = NC;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + p.nstages;
@@ -606,7 +603,7 @@ __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(c
     // memory first: they never depend on the previous kernel, so these loads overlap
     // the wait for the predecessor and for x.
     const int tid = threadIdx.x;
-    constexpr int nthr = kNumConsumerWarps * 32;
+    constexpr int nthr = NC * 32;
     const uint32_t rec0 = p.tile_rec[t0];
     const uint32_t nrec_cta = p.tile_rec[t1] - rec0;
     const uint32_t ntl = t1 - t0;
@@ -617,7 +614,7 @@ __global__ void __launch_bounds__(kThreadsTiled, kCtasPerSm) ecsr_tiled_kernel(c
 
     if (!x_bulk)
         for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
-    consumer_bar_sync();  // tile_rec_s (and a consumer-copied x) complete
+    consumer_bar_sync<NC>();  // tile_rec_s (and a consumer-copied x) complete
     if (!x_bulk && tid == 0) mbar_arrive(xbar);
     YGate gate{p.sync, &gate_target, !p.zero_y};
     mbar_wait(xbar, 0);
