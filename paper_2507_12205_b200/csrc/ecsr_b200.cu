@@ -122,6 +122,14 @@ double host_value(const void* vals, int dtype, int64_t i) {
 
 int elem_size(int dtype) { return dtype == ECSR_F64 ? 8 : dtype == ECSR_F32 ? 4 : 2; }
 
+// Per-tile work features (cost-model calibration, ecsr_b200_debug_ctafeat).
+struct TileFeat {
+    double rec[4] = {0, 0, 0, 0};    // records with g = 1, 2, 4, >= 8
+    double steps[4] = {0, 0, 0, 0};  // block-chunk steps (sum over blocks of chunks)
+    double bytes = 0;
+};
+inline int gclass(int g) { return g == 1 ? 0 : g == 2 ? 1 : g == 4 ? 2 : 3; }
+
 struct SetDesc {
     int32_t g = 0, v = 0;
     int64_t nb = 0, stored = 0, real = 0;
@@ -160,6 +168,8 @@ struct ecsr_dev {
     unsigned long long* d_sync = nullptr;  // zero-y grid-barrier generation counter
     bool lean = false;                     // every run uses a lean-kernel record variant
     int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
+    std::vector<TileFeat> tile_feat;       // per tile (cost-model calibration)
+    std::vector<uint32_t> cta_tile_h;      // host copy of the CTA tile ranges
     unsigned long long* d_trace = nullptr; // debug timeline (ECSR_B200_DEBUG & 4)
     int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
     // ordered reduction
@@ -313,6 +323,9 @@ int64_t group_record_bytes(const ecsr_host_set* sets, const GroupPlan& gp, bool 
 // delta/value loads, ~150 per record for header, reduce-scatter and emit; an SM
 // issues ~2.4 warp instructions per cycle in practice. HBM delivers ~23.6 B per
 // cycle per SM at the measured peak, so a tile costs the sum of both estimates.
+// (A fit of measured per-CTA times, scripts/calibrate_cost.py, gives ~1.72 cycles per
+// record byte for every g plus a per-record overhead; it balanced no better: the
+// remaining CTA spread is runtime variance.)
 double group_record_cost(const ecsr_host_set* sets, const GroupPlan& gp, bool wide) {
     const ecsr_host_set& s0 = sets[gp.blocks[0].first];
     const int g = s0.granularity, v = s0.vector_size;
@@ -401,11 +414,13 @@ void write_group_record(const ecsr_host_set* sets, const std::vector<SetDesc>& d
 void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<SetDesc>& desc,
                        int host_dtype, bool wide, std::vector<uint8_t>* arena,
                        std::vector<uint32_t>* tile_start16, std::vector<uint32_t>* tile_rec_start,
-                       std::vector<double>* tile_cost, int64_t* max_tile) {
+                       std::vector<double>* tile_cost, std::vector<TileFeat>* tile_feat,
+                       int64_t* max_tile) {
     arena->clear();
     tile_start16->clear();
     tile_rec_start->assign(1, 0u);
     tile_cost->clear();
+    tile_feat->clear();
     *max_tile = 0;
     // 1. plan records: P consecutive blocks of a (g, v) run; P halves while the run's
     //    widest block would make a record exceed kRecordCap
@@ -463,7 +478,13 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
             std::memcpy(base + 6, &p16, 2);
             int64_t off = hdr;
             double cost = 0;
+            TileFeat tf;
             for (size_t k = 0; k < n; ++k) {
+                const GroupPlan& gp = run[i + k];
+                const int gc = gclass(sets[gp.blocks[0].first].granularity);
+                tf.rec[gc] += 1;
+                for (auto& sb : gp.blocks) tf.steps[gc] += static_cast<double>(block_chunks(sets[sb.first], sb.second));
+                tf.bytes += static_cast<double>(group_record_bytes(sets, gp, wide));
                 const uint16_t off16 = static_cast<uint16_t>(off / 16);
                 std::memcpy(base + 8 + 2 * k, &off16, 2);
                 write_group_record(sets, desc, run[i + k], host_dtype, wide, base + off);
@@ -473,6 +494,7 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
             tile_start16->push_back(static_cast<uint32_t>(start / 16));
             tile_rec_start->push_back(tile_rec_start->back() + static_cast<uint32_t>(n));
             tile_cost->push_back(cost);
+            tile_feat->push_back(tf);
             *max_tile = std::max<int64_t>(*max_tile, hdr + bytes);
             i += n;
         }
@@ -763,7 +785,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
         std::vector<double> tcost;
         int64_t max_tile = 0;
         build_tiled_arena(sets, nsets, d->sets, host_value_dtype, wide, &arena, &tstart, &trec, &tcost,
-                          &max_tile);
+                          &d->tile_feat, &max_tile);
         // the lean kernel covers v = 4 runs with the default blocks-per-record and
         // g <= 8, and v = 1 runs of g = 1 (the reference's short set)
         d->lean = true;
@@ -814,6 +836,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 d->d_tile_start16 = dalloc_copy(tstart, &total, &err);
                 if (d->d_tile_start16) d->allocs.push_back(d->d_tile_start16);
             }
+            d->cta_tile_h = cta;
             if (err == cudaSuccess) {
                 d->d_cta_tile = dalloc_copy(cta, &total, &err);
                 if (d->d_cta_tile) d->allocs.push_back(d->d_cta_tile);
@@ -1093,6 +1116,25 @@ void ecsr_b200_free(ecsr_dev* d) { delete d; }
 int ecsr_b200_debug_trace(const ecsr_dev* d, unsigned long long* out, int64_t n) {
     if (!d || !d->d_trace) return fail(ECSR_ERR_VALUE, "no trace recorded");
     ECSR_CUDA(cudaMemcpy(out, d->d_trace, 8 * std::min<int64_t>(n, 16 * d->grid), cudaMemcpyDeviceToHost));
+    return ECSR_OK;
+}
+
+// Internal tuning aid: per CTA 9 doubles -- records and block-chunk steps for g = 1, 2,
+// 4, >= 8 (interleaved rec, steps) and record bytes -- of its static tile range.
+int ecsr_b200_debug_ctafeat(const ecsr_dev* d, double* out, int64_t n) {
+    if (!d || d->layout != 1) return fail(ECSR_ERR_VALUE, "no tiled layout");
+    for (int c = 0; c < d->grid && 9 * (c + 1) <= n; ++c) {
+        double f[9] = {0};
+        for (uint32_t t = d->cta_tile_h[c]; t < d->cta_tile_h[c + 1]; ++t) {
+            const TileFeat& tf = d->tile_feat[t];
+            for (int k = 0; k < 4; ++k) {
+                f[2 * k] += tf.rec[k];
+                f[2 * k + 1] += tf.steps[k];
+            }
+            f[8] += tf.bytes;
+        }
+        std::memcpy(out + 9 * c, f, sizeof f);
+    }
     return ECSR_OK;
 }
 
