@@ -169,7 +169,8 @@ struct ecsr_dev {
     bool lean = false;                     // every run uses a lean-kernel record variant
     int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
     std::vector<TileFeat> tile_feat;       // per tile (cost-model calibration)
-    std::vector<uint32_t> cta_tile_h;      // host copy of the CTA tile ranges
+    std::vector<uint32_t> cta_tile_h;      // host copy of the CTA tile boundaries
+    std::vector<uint32_t> cta_range_h;     // per block [lo, hi) (launch order)
     unsigned long long* d_trace = nullptr; // debug timeline (ECSR_B200_DEBUG & 4)
     int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
     // ordered reduction
@@ -837,8 +838,20 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 if (d->d_tile_start16) d->allocs.push_back(d->d_tile_start16);
             }
             d->cta_tile_h = cta;
+            // Co-resident CTAs of one SM are blocks b and b + sms (the block scheduler
+            // fills every SM once before doubling up). Contiguous ranges would give both
+            // the same relative position in row-stacked matrices (q|k|v, gate|up) and so
+            // the same set type; the second slot walks the ranges in reverse instead, so
+            // each SM pairs complementary work.
+            std::vector<uint32_t> ranges(2 * grid);
+            for (int b = 0; b < grid; ++b) {
+                const int r = (ctas_per_sm == 2 && b >= grid / 2) ? grid - 1 - (b - grid / 2) : b;
+                ranges[2 * b] = cta[r];
+                ranges[2 * b + 1] = cta[r + 1];
+            }
+            d->cta_range_h = ranges;
             if (err == cudaSuccess) {
-                d->d_cta_tile = dalloc_copy(cta, &total, &err);
+                d->d_cta_tile = dalloc_copy(ranges, &total, &err);
                 if (d->d_cta_tile) d->allocs.push_back(d->d_cta_tile);
             }
             if (err == cudaSuccess) {
@@ -1125,7 +1138,7 @@ int ecsr_b200_debug_ctafeat(const ecsr_dev* d, double* out, int64_t n) {
     if (!d || d->layout != 1) return fail(ECSR_ERR_VALUE, "no tiled layout");
     for (int c = 0; c < d->grid && 9 * (c + 1) <= n; ++c) {
         double f[9] = {0};
-        for (uint32_t t = d->cta_tile_h[c]; t < d->cta_tile_h[c + 1]; ++t) {
+        for (uint32_t t = d->cta_range_h[2 * c]; t < d->cta_range_h[2 * c + 1]; ++t) {
             const TileFeat& tf = d->tile_feat[t];
             for (int k = 0; k < 4; ++k) {
                 f[2 * k] += tf.rec[k];

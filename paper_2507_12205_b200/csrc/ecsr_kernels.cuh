@@ -44,7 +44,7 @@ constexpr uint32_t kTileRecCache = 256;  // per-CTA record prefix counts kept in
 struct TiledParams {
     const uint8_t* arena;          // block-major tiles, 16-B aligned
     const uint32_t* tile_start16;  // [ntiles + 1] tile offsets in 16-B units
-    const uint32_t* cta_tile;      // [grid + 1] first tile of each CTA
+    const uint32_t* cta_tile;      // [2 * grid] tile range [lo, hi) of each CTA
     const uint32_t* tile_rec;      // [ntiles + 1] record prefix counts
     const __half* x;               // [K]
     float* y;                      // [M]
@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t t0 = p.cta_tile[blockIdx.x];
-    const uint32_t t1 = p.cta_tile[blockIdx.x + 1];
+    const uint32_t t0 = p.cta_tile[2 * blockIdx.x];      // [t0, t1): this CTA's tiles
+    const uint32_t t1 = p.cta_tile[2 * blockIdx.x + 1];
     // x by one bulk copy when it is 16-B aligned and a multiple of 16 bytes
     const bool x_bulk = p.x_vec16 && (p.K & 7) == 0 && p.K > 0;
 
