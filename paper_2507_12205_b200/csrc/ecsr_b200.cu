@@ -802,7 +802,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         d->ctas_per_sm = ctas_per_sm;  // CTAs share the SM's 228 KB (1 KB reserved each)
         const int64_t cta_smem = ctas_per_sm == 1 ? lim.smem_optin : (lim.smem_per_sm / ctas_per_sm) - 1024;
-        const int64_t avail = cta_smem - 3072 - 16 * kMaxStages - xbytes;  // static smem + barriers
+        const int64_t avail = cta_smem - 4096 - 16 * kMaxStages - xbytes;  // static smem + barriers
         const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
         if (stage > kMaxStageBytes || nst < 2 || arena.size() / 16 >= (1ull << 32)) tiled = false;
         if (tiled) {
@@ -829,6 +829,41 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             while (c < grid) cta[c++] = static_cast<uint32_t>(ntiles);
             cta[grid] = static_cast<uint32_t>(ntiles);
             for (int i = 1; i <= grid; ++i) cta[i] = std::max(cta[i], cta[i - 1]);
+            // Within each CTA's range, tiles go longest record first (LPT): records are
+            // handed to warps in arena order, so the last ones of a CTA are short and the
+            // launch's tail shrinks. Unpack identifies blocks by slot, not position.
+            {
+                std::vector<uint32_t> order(ntiles);
+                for (int c2 = 0; c2 < grid; ++c2) {
+                    std::vector<uint32_t> ts;
+                    for (uint32_t t = cta[c2]; t < cta[c2 + 1]; ++t) ts.push_back(t);
+                    std::stable_sort(ts.begin(), ts.end(), [&](uint32_t x, uint32_t y) {
+                        const double cx = tcost[x] / std::max<uint32_t>(1, trec[x + 1] - trec[x]);
+                        const double cy = tcost[y] / std::max<uint32_t>(1, trec[y + 1] - trec[y]);
+                        return cx > cy;
+                    });
+                    std::copy(ts.begin(), ts.end(), order.begin() + cta[c2]);
+                }
+                std::vector<uint8_t> na;
+                na.reserve(arena.size());
+                std::vector<uint32_t> nts(ntiles + 1), ntr(ntiles + 1, 0);
+                std::vector<double> ntc(ntiles);
+                std::vector<TileFeat> ntf(ntiles);
+                for (int64_t i = 0; i < ntiles; ++i) {
+                    const uint32_t t = order[i];
+                    nts[i] = static_cast<uint32_t>(na.size() / 16);
+                    na.insert(na.end(), arena.begin() + 16ull * tstart[t], arena.begin() + 16ull * tstart[t + 1]);
+                    ntr[i + 1] = ntr[i] + (trec[t + 1] - trec[t]);
+                    ntc[i] = tcost[t];
+                    ntf[i] = d->tile_feat[t];
+                }
+                nts[ntiles] = static_cast<uint32_t>(na.size() / 16);
+                arena.swap(na);
+                tstart.swap(nts);
+                trec.swap(ntr);
+                tcost.swap(ntc);
+                d->tile_feat.swap(ntf);
+            }
             cudaError_t err = cudaSuccess;
             d->arena_bytes = static_cast<int64_t>(arena.size());
             d->d_arena = dalloc_copy(arena, &total, &err);
@@ -1012,13 +1047,31 @@ int ecsr_b200_unpack(const ecsr_dev* d, ecsr_out_set* out, int32_t nsets, int32_
         std::vector<uint32_t> tstart(d->ntiles + 1);
         ECSR_CUDA(cudaMemcpy(arena.data(), d->d_arena, d->arena_bytes, cudaMemcpyDeviceToHost));
         ECSR_CUDA(cudaMemcpy(tstart.data(), d->d_tile_start16, 4 * (d->ntiles + 1), cudaMemcpyDeviceToHost));
-        int si = 0;
-        int64_t b = 0;
-        while (si < nsets && d->sets[si].nb == 0) {
-            out[si].block_indptr[0] = 0;
-            ++si;
-        }
-        // Walk group records in order; every block restores its reference arrays.
+        // Records may sit in any order (the packer orders each CTA's tiles longest
+        // record first); every block is identified by its ordered-mode slot, which is
+        // unique: slot = set.slot0 + block * g. Pass 1 finds every block's record and
+        // chunk count, pass 2 restores the reference arrays.
+        struct Ref {
+            const uint8_t* rec = nullptr;
+            int bk = 0;
+            int64_t nch = -1;
+        };
+        std::vector<std::vector<Ref>> refs(nsets);
+        for (int si = 0; si < nsets; ++si) refs[si].resize(d->sets[si].nb);
+        auto set_of_slot = [&](uint32_t slot) -> int {
+            int lo = 0, hi = nsets - 1, ans = -1;
+            while (lo <= hi) {  // last set with slot0 <= slot (sets are in slot order)
+                const int mid = (lo + hi) / 2;
+                if (d->sets[mid].slot0 <= slot) {
+                    ans = mid;
+                    lo = mid + 1;
+                } else {
+                    hi = mid - 1;
+                }
+            }
+            while (ans >= 0 && d->sets[ans].nb == 0) --ans;  // empty sets own no slots
+            return ans;
+        };
         for (int64_t t = 0; t < d->ntiles; ++t) {
             const uint8_t* tile = arena.data() + 16ull * tstart[t];
             uint32_t nrec;
@@ -1029,62 +1082,76 @@ int ecsr_b200_unpack(const ecsr_dev* d, ecsr_out_set* out, int32_t nsets, int32_
                 const uint8_t* r = tile + 16 * off16;
                 uint16_t nmin;
                 std::memcpy(&nmin, r + 48, 2);
-                const int g = r[50], v = r[51], nb = r[52], P = r[54];
-                const int esz = d->wide ? 4 : 2;
+                const int g = r[50], v = r[51], nb = r[52];
+                for (int bk = 0; bk < nb; ++bk) {
+                    uint32_t slot;
+                    std::memcpy(&slot, r + 4 * bk, 4);
+                    const int si = set_of_slot(slot);
+                    if (si < 0) return fail(ECSR_ERR_CONTAINER, "record slot outside every set");
+                    const SetDesc& sd = d->sets[si];
+                    if (g != sd.g || v != sd.v) return fail(ECSR_ERR_CONTAINER, "arena/set descriptor mismatch");
+                    const int64_t blk = (static_cast<int64_t>(slot) - sd.slot0) / g;
+                    if (blk >= sd.nb || refs[si][blk].nch >= 0)
+                        return fail(ECSR_ERR_CONTAINER, "record slot out of range or repeated");
+                    uint16_t nt;
+                    std::memcpy(&nt, r + 32 + 2 * bk, 2);
+                    refs[si][blk] = Ref{r, bk, static_cast<int64_t>(nmin) + nt};
+                }
+            }
+        }
+        const int esz = d->wide ? 4 : 2;
+        for (int si = 0; si < nsets; ++si) {
+            const SetDesc& sd = d->sets[si];
+            ecsr_out_set& o = out[si];
+            o.block_indptr[0] = 0;
+            for (int64_t b = 0; b < sd.nb; ++b) {
+                const Ref& rf = refs[si][b];
+                if (rf.nch < 0) return fail(ECSR_ERR_CONTAINER, "arena holds fewer blocks than sets");
+                const uint8_t* r = rf.rec;
+                const int g = r[50], v = r[51], P = r[54], bk = rf.bk;
+                uint16_t nmin;
+                std::memcpy(&nmin, r + 48, 2);
                 const uint8_t* q = r + ecsr::group_header_bytes(g, P);
                 const uint8_t* body = q + 32 * P * esz;
                 const int64_t dch = 32 * v, vch = 32 * v * g;
                 const int64_t S = P * (dch + 2 * vch);
-                const uint8_t* tail = body + nmin * S;
-                for (int bk = 0; bk < nb; ++bk) {
-                    if (si >= nsets) return fail(ECSR_ERR_CONTAINER, "arena holds more blocks than sets");
-                    const SetDesc& sd = d->sets[si];
-                    ecsr_out_set& o = out[si];
-                    if (g != sd.g || v != sd.v) return fail(ECSR_ERR_CONTAINER, "arena/set descriptor mismatch");
+                const uint8_t* tail = body + nmin * S;  // block bk's tail follows blocks < bk
+                for (int pb = 0; pb < bk; ++pb) {
                     uint16_t nt;
-                    std::memcpy(&nt, r + 32 + 2 * bk, 2);
-                    const int64_t nch = nmin + nt;
-                    if (b == 0) o.block_indptr[0] = 0;
-                    o.block_indptr[b + 1] = o.block_indptr[b] + nch * dch;
-                    std::memcpy(o.row_indices + b * g, r + 64 + 4 * g * bk, 4 * g);
-                    for (int l = 0; l < 32; ++l) {
-                        uint32_t bv = 0;
-                        std::memcpy(&bv, q + (l * P + bk) * esz, esz);
-                        o.base_indices[b * 32 + l] = bv;
+                    std::memcpy(&nt, r + 32 + 2 * pb, 2);
+                    tail += static_cast<int64_t>(nt) * (dch + 2 * vch);
+                }
+                const int64_t nch = rf.nch;
+                o.block_indptr[b + 1] = o.block_indptr[b] + nch * dch;
+                std::memcpy(o.row_indices + b * g, r + 64 + 4 * g * bk, 4 * g);
+                for (int l = 0; l < 32; ++l) {
+                    uint32_t bv = 0;
+                    std::memcpy(&bv, q + (l * P + bk) * esz, esz);
+                    o.base_indices[b * 32 + l] = bv;
+                }
+                const int64_t st0 = o.block_indptr[b];
+                for (int64_t c = 0; c < nch; ++c) {
+                    const uint8_t* dp;
+                    const uint8_t* vp;
+                    if (c < nmin) {
+                        dp = body + c * S + bk * dch;
+                        vp = body + c * S + P * dch + bk * 2 * vch;
+                    } else {
+                        dp = tail;
+                        vp = tail + dch;
+                        tail += dch + 2 * vch;
                     }
-                    const int64_t st0 = o.block_indptr[b];
-                    for (int64_t c = 0; c < nch; ++c) {
-                        const uint8_t* dp;
-                        const uint8_t* vp;
-                        if (c < nmin) {
-                            dp = body + c * S + bk * dch;
-                            vp = body + c * S + P * dch + bk * 2 * vch;
-                        } else {
-                            dp = tail;
-                            vp = tail + dch;
-                            tail += dch + 2 * vch;
-                        }
-                        for (int64_t i = 0; i < dch; ++i) o.delta_indices[st0 + c * dch + i] = dp[i];
-                        for (int64_t i = 0; i < vch; ++i) {
-                            uint16_t h;
-                            std::memcpy(&h, vp + 2 * i, 2);
-                            const int64_t at = (st0 + c * dch) * g + i;
-                            if (out_value_dtype == ECSR_F16) static_cast<uint16_t*>(o.block_values)[at] = h;
-                            else store_value(o.block_values, out_value_dtype, at, f16_to_f32(h));
-                        }
-                    }
-                    if (++b == sd.nb) {
-                        b = 0;
-                        ++si;
-                        while (si < nsets && d->sets[si].nb == 0) {
-                            out[si].block_indptr[0] = 0;
-                            ++si;
-                        }
+                    for (int64_t i = 0; i < dch; ++i) o.delta_indices[st0 + c * dch + i] = dp[i];
+                    for (int64_t i = 0; i < vch; ++i) {
+                        uint16_t h;
+                        std::memcpy(&h, vp + 2 * i, 2);
+                        const int64_t at = (st0 + c * dch) * g + i;
+                        if (out_value_dtype == ECSR_F16) static_cast<uint16_t*>(o.block_values)[at] = h;
+                        else store_value(o.block_values, out_value_dtype, at, f16_to_f32(h));
                     }
                 }
             }
         }
-        if (si != nsets) return fail(ECSR_ERR_CONTAINER, "arena holds fewer blocks than sets");
         return ECSR_OK;
     }
     // generic layout: copy the reference arrays back
