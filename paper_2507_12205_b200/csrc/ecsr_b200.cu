@@ -298,6 +298,16 @@ struct GroupPlan {
 // A record of P blocks must fit a ring stage next to x: runs of very wide blocks
 // (large K) get fewer blocks per record.
 constexpr int64_t kRecordCap = 24 * 1024;
+// A ring stage holds whole records, so records much larger than a tile leave consumer
+// warps without work (fewer resident records than warps): a run's AVERAGE record is
+// also held to ~rec_cap() = half a tile (ECSR_B200_RECCAP overrides, for tuning).
+int64_t rec_cap() {
+    static int64_t env = [] {
+        const char* e = std::getenv("ECSR_B200_RECCAP");
+        return e ? static_cast<int64_t>(std::max(512, std::atoi(e))) : int64_t{0};
+    }();
+    return env ? env : tile_target() / 2;
+}
 
 int group_p(int g) { return g > 8 ? 1 : ecsr::group_blocks(g); }
 
@@ -433,13 +443,20 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
                sets[se].vector_size == sets[si].vector_size)
             ++se;
         const int g = sets[si].granularity, v = sets[si].vector_size;
-        int64_t widest = 0;
+        int64_t widest = 0, nblk = 0, sum_chunks = 0;
         for (int k = si; k < se; ++k)
-            for (int64_t b = 0; b < sets[k].num_blocks; ++b) widest = std::max(widest, block_chunks(sets[k], b));
+            for (int64_t b = 0; b < sets[k].num_blocks; ++b) {
+                widest = std::max(widest, block_chunks(sets[k], b));
+                sum_chunks += block_chunks(sets[k], b);
+                ++nblk;
+            }
         const int64_t chunk = 32 * v + 64 * v * g;
+        const double mean = nblk ? static_cast<double>(sum_chunks) / static_cast<double>(nblk) : 0.0;
         int P = group_p(g);
+        auto hdr_p = [&](int q) { return ecsr::group_header_bytes(g, q) + (wide ? 128 : 64) * q; };
         while (v == 4 && P > 1 &&  // the kernel has reduced-P variants for v = 4 only
-               ecsr::group_header_bytes(g, P) + (wide ? 128 : 64) * P + P * widest * chunk > kRecordCap)
+               (hdr_p(P) + P * widest * chunk > kRecordCap ||
+                static_cast<double>(hdr_p(P)) + P * mean * static_cast<double>(chunk) > static_cast<double>(rec_cap())))
             P /= 2;
         runs.emplace_back();
         for (int k = si; k < se; ++k)
@@ -787,8 +804,8 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
         int64_t max_tile = 0;
         build_tiled_arena(sets, nsets, d->sets, host_value_dtype, wide, &arena, &tstart, &trec, &tcost,
                           &d->tile_feat, &max_tile);
-        // the lean kernel covers v = 4 runs with the default blocks-per-record and
-        // g <= 8, and v = 1 runs of g = 1 (the reference's short set)
+        // the lean kernel covers v = 4 runs with the default blocks-per-record (or half
+        // of it for g = 2, down to a quarter for g = 1) and g <= 8, and v = 1 runs of g = 1 (the reference's short set)
         d->lean = true;
         for (int64_t t = 0; t + 1 < static_cast<int64_t>(tstart.size()); ++t) {
             const uint8_t* th = arena.data() + 16ull * tstart[t];
@@ -796,7 +813,9 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             std::memcpy(&gv, th + 4, 2);
             std::memcpy(&pp, th + 6, 2);
             const int g = gv >> 8, v = gv & 0xff;
-            const bool ok = (v == 4 && g <= 8 && pp == group_p(g)) || (v == 1 && g == 1);
+            const bool ok = (v == 4 && g <= 8 &&
+                             (pp == group_p(g) || (g <= 2 && 2 * pp == group_p(g)) || (g == 1 && 4 * pp == group_p(g)))) ||
+                            (v == 1 && g == 1);
             if (!ok) d->lean = false;
         }
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);

@@ -430,7 +430,7 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
 }
 
 // kFull: every (g, v, P) record variant; otherwise only the common ones (v = 4 with
-// the default P, v = 1 with g = 1) -- a smaller kernel body keeps the instruction
+// the default P, or half of it for g = 2, or down to a quarter for g = 1; v = 1 with g = 1) -- a smaller kernel body keeps the instruction
 // cache warm; the packer picks the lean kernel when the container needs nothing else.
 template <bool kFull>
 __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P, uint32_t xs, int lane,
@@ -443,8 +443,15 @@ __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P
             return;
         }
         switch (g) {
-            case 1: tiled_group_record<1, 4, group_blocks(1)>(r, xs, lane, p, gate); break;
-            case 2: tiled_group_record<2, 4, group_blocks(2)>(r, xs, lane, p, gate); break;
+            case 1:
+                if (P == group_blocks(1)) tiled_group_record<1, 4, group_blocks(1)>(r, xs, lane, p, gate);
+                else if (P == group_blocks(1) / 2) tiled_group_record<1, 4, group_blocks(1) / 2>(r, xs, lane, p, gate);
+                else tiled_group_record<1, 4, group_blocks(1) / 4>(r, xs, lane, p, gate);
+                break;
+            case 2:
+                if (P == group_blocks(2)) tiled_group_record<2, 4, group_blocks(2)>(r, xs, lane, p, gate);
+                else tiled_group_record<2, 4, group_blocks(2) / 2>(r, xs, lane, p, gate);
+                break;
             case 4: tiled_group_record<4, 4, group_blocks(4)>(r, xs, lane, p, gate); break;
             default: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate); break;
         }
