@@ -329,21 +329,16 @@ int64_t group_record_bytes(const ecsr_host_set* sets, const GroupPlan& gp, bool 
     return ecsr::group_header_bytes(g, P) + (wide ? 128 : 64) * P + chunk * (nmin * P + tails);
 }
 
-// Consumer-cycle estimate of one record on one SM (tile balancing): shared-memory
-// walks issue ~(3 + g) instructions per column per lane, ~4 per chunk for the
-// delta/value loads, ~150 per record for header, reduce-scatter and emit; an SM
-// issues ~2.4 warp instructions per cycle in practice. HBM delivers ~23.6 B per
-// cycle per SM at the measured peak, so a tile costs the sum of both estimates.
-// (A fit of measured per-CTA times, scripts/calibrate_cost.py, gives ~1.72 cycles per
-// record byte for every g plus a per-record overhead; it balanced no better: the
-// remaining CTA spread is runtime variance.)
+// Consumer-time estimate of one record (tile balancing), fitted to measured per-CTA
+// times of the bench layer (scripts/calibrate_cost.py, ECSR_CAL_DUMP; median error 3 %):
+// ~151 CTA cycles per record (dispatch, stage lookup, header, reduce-scatter, emit),
+// ~8 per block-chunk step and ~0.057 per byte. The per-record term is as large as the
+// byte term for the small g = 2 / g = 4 records, so tiles of many small records
+// weigh more than their bytes.
 double group_record_cost(const ecsr_host_set* sets, const GroupPlan& gp, bool wide) {
-    const ecsr_host_set& s0 = sets[gp.blocks[0].first];
-    const int g = s0.granularity, v = s0.vector_size;
     double steps = 0;
     for (auto& sb : gp.blocks) steps += static_cast<double>(block_chunks(sets[sb.first], sb.second));
-    const double instr = 150.0 + steps * (v * (3.0 + g) + 4.0);
-    return instr / 2.4 + static_cast<double>(group_record_bytes(sets, gp, wide)) / 23.6;
+    return 151.0 + 8.0 * steps + 0.057 * static_cast<double>(group_record_bytes(sets, gp, wide));
 }
 
 void write_group_record(const ecsr_host_set* sets, const std::vector<SetDesc>& desc, const GroupPlan& gp,

@@ -534,6 +534,11 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     }
     __syncthreads();
     ECSR_TRACE(0, threadIdx.x == 0);
+    if (p.trace && threadIdx.x == 0) {
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[blockIdx.x * 16 + 12] = smid;
+    }
 
     if (warp == kProducerWarp) {
         // The whole warp runs the producer loop: lanes < nstages poll the stage pool in

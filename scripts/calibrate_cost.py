@@ -35,6 +35,8 @@ for ln, names in bench.LAUNCHES:
     work = (t[:, 6] - t[:, 2]) / 1e3 * 1965.0  # cycles from x ready to the CTA's last warp
     X.append(ft.reshape(grid, 9))
     Y.append(work)
+    if os.environ.get("ECSR_CAL_DUMP"):
+        np.savez(os.path.join(os.environ["ECSR_CAL_DUMP"], f"cal_{ln}.npz"), trace=t, feat=ft.reshape(grid, 9))
     print(ln, "CTA work cycles: min %.0f med %.0f max %.0f" % (work.min(), np.median(work), work.max()))
 X = np.concatenate(X)
 Y = np.concatenate(Y)

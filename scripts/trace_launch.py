@@ -31,3 +31,20 @@ end = (t[:, 6] - t0) / 1e3
 print("CTA end by index (8 per row):")
 for c in range(0, grid, 16):
     print("  ", " ".join(f"{e:5.1f}" for e in end[c:c + 16]))
+
+sm = t[:, 12]
+per_sm = {}
+for c in range(grid):
+    per_sm.setdefault(int(sm[c]), []).append(end[c])
+sms = sorted(per_sm)
+sm_end = np.array([max(per_sm[s]) for s in sms])
+print("SM end (max over its CTAs) by smid (16 per row):")
+for i in range(0, len(sms), 16):
+    print("  ", " ".join(f"{sm_end[j]:5.1f}" for j in range(i, min(i + 16, len(sms)))))
+# does the slowness follow the SM or the work? correlate with per-CTA tile count
+nt = t[:, 11]
+print("corr(end, ntiles) =", float(np.corrcoef(end, nt)[0, 1]))
+if t[:, 10].sum() > 0:  # ECSR_TRACE_CYCLES build: consumer wait vs work cycles
+    wait, work, nrec = t[:, 8].sum(), t[:, 9].sum(), t[:, 10].sum()
+    print(f"consumer cycles: wait {wait / (wait + work):.1%} of wait+work; "
+          f"work per record {work / nrec:.0f}, wait per record {wait / nrec:.0f} cycles; records {nrec}")
