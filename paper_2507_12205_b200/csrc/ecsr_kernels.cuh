@@ -318,12 +318,16 @@ template <int G, int V, int P>
 __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const TiledParams& p,
                                                    YGate& gate) {
     constexpr int NACC = P * G;
+    constexpr int kStride = 32 / NACC;
+    const int a = lane / kStride;  // accumulator a after the reduce-scatter: block a / G, row a % G
+    const int blk = a / G, k = a % G;
+    // header, lane bases and the lane's output row (or partial slot) are independent
+    // shared loads: issue them together so their latencies overlap
+    const uint32_t q = r + group_header_bytes(G, P);
     uint32_t m[2];
     lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
-    const uint32_t nmin = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
-    if (!present) return;  // zero-width blocks only (_speedups.pyx:105-106)
-    const bool has_tail = (m[1] >> 24) != 0;  // header byte 55
-    const uint32_t q = r + group_header_bytes(G, P);
+    uint32_t out_idx;
+    lds_bytes<4>(p.ordered ? r + 4 * blk : r + 64 + 4 * (blk * G + k), &out_idx);
     uint32_t xa[P];
     if (p.wide) {
         uint32_t bb[P];
@@ -336,6 +340,9 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
 #pragma unroll
         for (int b = 0; b < P; ++b) xa[b] = xs + 2u * ((bb[b >> 1] >> (16 * (b & 1))) & 0xffffu);
     }
+    const uint32_t nmin = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
+    if (!present) return;  // zero-width blocks only (_speedups.pyx:105-106)
+    const bool has_tail = (m[1] >> 24) != 0;  // header byte 55
     constexpr uint32_t DCH = 32 * V, VCH = 64 * V * G, LV = 2 * V * G;  // bytes
     constexpr int NW = (LV + 3) / 4;
     uint32_t ptr = q + (p.wide ? 128u : 64u) * P;
@@ -377,10 +384,12 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
     }
     const float sum = warp_reduce_scatter<NACC>(acc, lane);
     if (!p.ordered) gate.pass(lane);
-    constexpr int kStride = 32 / NACC;
-    const int a = lane / kStride;  // accumulator a: block a / G, row a % G
-    const int blk = a / G, k = a % G;
-    if ((lane & (kStride - 1)) == 0 && ((present >> blk) & 1u)) emit_row(r, G, P, blk, k, sum, p);
+    if ((lane & (kStride - 1)) == 0 && ((present >> blk) & 1u)) {
+        if (p.ordered)
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(p.partials + out_idx + k), "f"(sum) : "memory");
+        else
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p.y + out_idx), "f"(sum) : "memory");
+    }
 }
 
 // A single-block record of g = 8 * passes rows (g in {16, 32}): one walk per pass of
