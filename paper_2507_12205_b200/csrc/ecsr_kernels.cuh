@@ -214,24 +214,37 @@ __host__ __device__ constexpr int header_bytes() {
 
 // Per-warp state of the zero-y grid barrier: REDs into y may only start once every
 // CTA has zeroed its slice of y (see ecsr_tiled_kernel).
-// The CTA's arrival (producer warp, lane 1) publishes target + 1 in shared memory
-// (`target_smem`, 0 = not yet); consumers read it lazily at their first red.
+// The CTA's arrival (producer warp) publishes target + 1 in shared memory
+// (`target_smem`, 0 = not yet). The first consumer warp of the CTA to reach the gate
+// (shared `state` 0 -> 1) polls the grid counter with acquire loads and then releases
+// state = 2 at CTA scope; the other warps only watch the shared word, so a CTA pays
+// one loaded-L2 round trip instead of one per warp.
 struct YGate {
     const unsigned long long* counter;
     const unsigned long long* target_smem;
+    uint32_t* state;
     bool open;
     __device__ __forceinline__ void pass(int lane) {
         if (open) return;
         if (lane == 0) {
-            unsigned long long tgt;
-            do {
-                asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(tgt) : "r"(smem_addr(target_smem)) : "memory");
-            } while (tgt == 0);
-            --tgt;
-            unsigned long long v;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
-            } while (static_cast<long long>(v - tgt) < 0);
+            uint32_t st = atomicCAS(state, 0u, 1u);
+            if (st == 0u) {
+                unsigned long long tgt;
+                do {
+                    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(tgt) : "r"(smem_addr(target_smem)) : "memory");
+                } while (tgt == 0);
+                --tgt;
+                unsigned long long v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+                } while (static_cast<long long>(v - tgt) < 0);
+                asm volatile("st.release.cta.shared.u32 [%0], 2;" ::"r"(smem_addr(state)) : "memory");
+            } else {
+                while (st != 2u) {
+                    __nanosleep(32);
+                    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(st) : "r"(smem_addr(state)) : "memory");
+                }
+            }
         }
         __syncwarp();
         open = true;
@@ -512,6 +525,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     uint8_t* stages = smem + ((16 * p.nstages + 8 + 127) & ~127);
     __half* xs = reinterpret_cast<__half*>(stages + p.nstages * p.stage_bytes);
     __shared__ unsigned long long gate_target;
+    __shared__ uint32_t gate_state;                 // 0 closed, 1 a warp polls, 2 open
     __shared__ uint32_t rec_next;                   // dynamic record scheduler
     __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per ring stage
     // The stages form a pool, not an in-order ring: the producer refills whichever stage
@@ -539,6 +553,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         mbar_init(xbar, 1);
         rec_next = 0;
         gate_target = 0;
+        gate_state = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -637,7 +652,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
     consumer_bar_sync<NC>();  // tile_rec_s (and a consumer-copied x) complete
     if (!x_bulk && tid == 0) mbar_arrive(xbar);
-    YGate gate{p.sync, &gate_target, !p.zero_y};
+    YGate gate{p.sync, &gate_target, &gate_state, !p.zero_y};
     mbar_wait(xbar, 0);
     ECSR_TRACE(2, threadIdx.x == 0);
 
