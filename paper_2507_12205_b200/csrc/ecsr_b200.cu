@@ -301,12 +301,13 @@ constexpr int64_t kRecordCap = 24 * 1024;
 // A ring stage holds whole records, so records much larger than a tile leave consumer
 // warps without work (fewer resident records than warps): a run's AVERAGE record is
 // also held to ~rec_cap() = half a tile (ECSR_B200_RECCAP overrides, for tuning).
-int64_t rec_cap() {
-    static int64_t env = [] {
-        const char* e = std::getenv("ECSR_B200_RECCAP");
-        return e ? static_cast<int64_t>(std::max(512, std::atoi(e))) : int64_t{0};
-    }();
-    return env ? env : tile_target() / 2;
+int64_t rec_max() {  // hard record-size cap (ECSR_B200_RECMAX overrides, for tuning)
+    const char* e = std::getenv("ECSR_B200_RECMAX");
+    return e ? static_cast<int64_t>(std::max(512, std::atoi(e))) : kRecordCap;
+}
+int64_t rec_cap() {  // read at every pack (tuning sweeps change it between packs)
+    const char* e = std::getenv("ECSR_B200_RECCAP");
+    return e ? static_cast<int64_t>(std::max(512, std::atoi(e))) : tile_target() / 2;
 }
 
 int group_p(int g) { return g > 8 ? 1 : ecsr::group_blocks(g); }
@@ -450,7 +451,7 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
         int P = group_p(g);
         auto hdr_p = [&](int q) { return ecsr::group_header_bytes(g, q) + (wide ? 128 : 64) * q; };
         while (v == 4 && P > 1 &&  // the kernel has reduced-P variants for v = 4 only
-               (hdr_p(P) + P * widest * chunk > kRecordCap ||
+               (hdr_p(P) + P * widest * chunk > rec_max() ||
                 static_cast<double>(hdr_p(P)) + P * mean * static_cast<double>(chunk) > static_cast<double>(rec_cap())))
             P /= 2;
         runs.emplace_back();
@@ -792,7 +793,16 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
     if (tiled) {
         static std::mutex tile_mu;  // the packer is host code; serialise the tile default
         std::lock_guard<std::mutex> lock(tile_mu);
-        g_tile_default = ctas_per_sm == 2 ? 16384 : 32768;
+        // The stage pool fills the CTA's shared memory: stages of ~16 KB (2 CTAs/SM) or
+        // ~32 KB (1 CTA), stretched so that a whole number of them uses all of it
+        // (more bytes in flight per SM; e.g. 5 x 18.3 KB instead of 5 x 16 KB at K = 8192).
+        const int64_t cta_smem = ctas_per_sm == 1 ? lim.smem_optin : (lim.smem_per_sm / ctas_per_sm) - 1024;
+        const int64_t avail = cta_smem - 4096 - 16 * kMaxStages - xbytes;  // static smem + barriers
+        {
+            const int64_t base = ctas_per_sm == 2 ? 16384 : 32768;
+            const int64_t n0 = std::min<int64_t>(kMaxStages, std::max<int64_t>(2, avail / base));
+            g_tile_default = static_cast<int>(std::max<int64_t>(4096, (avail / n0) / 128 * 128));
+        }
         std::vector<uint8_t> arena;
         std::vector<uint32_t> tstart, trec;
         std::vector<double> tcost;
@@ -815,8 +825,6 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
         }
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         d->ctas_per_sm = ctas_per_sm;  // CTAs share the SM's 228 KB (1 KB reserved each)
-        const int64_t cta_smem = ctas_per_sm == 1 ? lim.smem_optin : (lim.smem_per_sm / ctas_per_sm) - 1024;
-        const int64_t avail = cta_smem - 4096 - 16 * kMaxStages - xbytes;  // static smem + barriers
         const int64_t nst = std::min<int64_t>(kMaxStages, avail / std::max<int64_t>(stage, 1));
         if (stage > kMaxStageBytes || nst < 2 || arena.size() / 16 >= (1ull << 32)) tiled = false;
         if (tiled) {
