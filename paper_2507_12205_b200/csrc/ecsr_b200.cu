@@ -138,6 +138,34 @@ struct SetDesc {
     int64_t base_off = 0, indptr_off = 0, col_off = 0, val_off = 0;
 };
 
+// Contiguous tile ranges [cta[c], cta[c+1]) of ~equal summed cost (a tile goes to the
+// range holding its cost midpoint).
+std::vector<uint32_t> balanced_ranges(const std::vector<double>& tcost, int grid) {
+    const int64_t ntiles = static_cast<int64_t>(tcost.size());
+    std::vector<uint32_t> cta(grid + 1, 0);
+    std::vector<double> cum(ntiles + 1, 0.0);
+    for (int64_t t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + tcost[t];
+    const double total_cost = cum[ntiles];
+    int c = 1;
+    for (int64_t t = 0; t < ntiles && c < grid; ++t) {
+        const double mid = 0.5 * (cum[t] + cum[t + 1]);
+        while (c < grid && mid >= total_cost * c / grid) cta[c++] = static_cast<uint32_t>(t);
+    }
+    while (c < grid) cta[c++] = static_cast<uint32_t>(ntiles);
+    cta[grid] = static_cast<uint32_t>(ntiles);
+    for (int i = 1; i <= grid; ++i) cta[i] = std::max(cta[i], cta[i - 1]);
+    return cta;
+}
+
+// Block b's range index: co-resident CTAs of one SM are blocks b and b + grid/2 (the
+// block scheduler fills every SM once before doubling up). Contiguous ranges would give
+// both the same relative position in row-stacked matrices (q|k|v, gate|up) and so the
+// same set type; the second slot walks the ranges in reverse instead, so each SM pairs
+// complementary work.
+int range_of_block(int b, int grid, int ctas_per_sm) {
+    return (ctas_per_sm == 2 && b >= grid / 2) ? grid - 1 - (b - grid / 2) : b;
+}
+
 template <typename T>
 T* dalloc_copy(const std::vector<T>& h, int64_t* total, cudaError_t* err) {
     T* d = nullptr;
@@ -838,19 +866,8 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             const int grid =
                 static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t{lim.sms} * ctas_per_sm, ntiles)));
             d->grid = grid;
-            // cost-balanced contiguous tile ranges (HBM bytes + consumer issue estimate)
-            std::vector<uint32_t> cta(grid + 1, 0);
-            std::vector<double> cum(ntiles + 1, 0.0);
-            for (int64_t t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + tcost[t];
-            const double total_cost = cum[ntiles];
-            int c = 1;
-            for (int64_t t = 0; t < ntiles && c < grid; ++t) {
-                const double mid = 0.5 * (cum[t] + cum[t + 1]);
-                while (c < grid && mid >= total_cost * c / grid) cta[c++] = static_cast<uint32_t>(t);
-            }
-            while (c < grid) cta[c++] = static_cast<uint32_t>(ntiles);
-            cta[grid] = static_cast<uint32_t>(ntiles);
-            for (int i = 1; i <= grid; ++i) cta[i] = std::max(cta[i], cta[i - 1]);
+            // cost-balanced contiguous tile ranges (fitted consumer-time model)
+            const std::vector<uint32_t> cta = balanced_ranges(tcost, grid);
             // Within each CTA's range, tiles go longest record first (LPT): records are
             // handed to warps in arena order, so the last ones of a CTA are short and the
             // launch's tail shrinks. Unpack identifies blocks by slot, not position.
@@ -895,14 +912,9 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 if (d->d_tile_start16) d->allocs.push_back(d->d_tile_start16);
             }
             d->cta_tile_h = cta;
-            // Co-resident CTAs of one SM are blocks b and b + sms (the block scheduler
-            // fills every SM once before doubling up). Contiguous ranges would give both
-            // the same relative position in row-stacked matrices (q|k|v, gate|up) and so
-            // the same set type; the second slot walks the ranges in reverse instead, so
-            // each SM pairs complementary work.
             std::vector<uint32_t> ranges(2 * grid);
             for (int b = 0; b < grid; ++b) {
-                const int r = (ctas_per_sm == 2 && b >= grid / 2) ? grid - 1 - (b - grid / 2) : b;
+                const int r = range_of_block(b, grid, ctas_per_sm);
                 ranges[2 * b] = cta[r];
                 ranges[2 * b + 1] = cta[r + 1];
             }
@@ -989,10 +1001,12 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
                 ECSR_CUDA(cudaMalloc(&dm->d_trace, 8 * 16 * d->grid));
                 dm->allocs.push_back(dm->d_trace);
             }
-            std::vector<unsigned long long> init(16 * d->grid, 0ull);
-            for (int c = 0; c < d->grid; ++c) init[16 * c + 7] = ~0ull;
-            ECSR_CUDA(cudaMemcpyAsync(dm->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice, st));
-            ECSR_CUDA(cudaStreamSynchronize(st));
+            if (!(debug_flags() & 8)) {  // 8: the caller resets (back-to-back traced launches)
+                std::vector<unsigned long long> init(16 * d->grid, 0ull);
+                for (int c = 0; c < d->grid; ++c) init[16 * c + 7] = ~0ull;
+                ECSR_CUDA(cudaMemcpyAsync(dm->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice, st));
+                ECSR_CUDA(cudaStreamSynchronize(st));
+            }
             p.trace = dm->d_trace;
         }
         p.wide = d->wide;
@@ -1218,6 +1232,19 @@ void ecsr_b200_free(ecsr_dev* d) { delete d; }
 int ecsr_b200_debug_trace(const ecsr_dev* d, unsigned long long* out, int64_t n) {
     if (!d || !d->d_trace) return fail(ECSR_ERR_VALUE, "no trace recorded");
     ECSR_CUDA(cudaMemcpy(out, d->d_trace, 8 * std::min<int64_t>(n, 16 * d->grid), cudaMemcpyDeviceToHost));
+    return ECSR_OK;
+}
+
+// Internal tuning aid: clear the trace buffer (after one traced launch allocated it).
+int ecsr_b200_debug_trace_reset(ecsr_dev* d) {
+    if (!d || d->layout != 1) return fail(ECSR_ERR_VALUE, "no tiled layout");
+    if (!d->d_trace) {
+        ECSR_CUDA(cudaMalloc(&d->d_trace, 8 * 16 * d->grid));
+        d->allocs.push_back(d->d_trace);
+    }
+    std::vector<unsigned long long> init(16 * d->grid, 0ull);
+    for (int c = 0; c < d->grid; ++c) init[16 * c + 7] = ~0ull;
+    ECSR_CUDA(cudaMemcpy(d->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice));
     return ECSR_OK;
 }
 
