@@ -118,6 +118,29 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
  * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream). */
 int ecsr_b200_spmv(const ecsr_dev* dev, const void* x, void* y, int32_t mode, void* stream);
 
+/* .ecsr wire format (storage.py:389-483) straight to a device handle, no numpy round trip
+ * (SURVEY.md §8(f) #3). ecsr_b200_parse parses and shape-checks a blob on the host only,
+ * rejecting corruption with the reference's ContainerError (code 1) and message: bad
+ * magic, version, value width / precision tag, delta width, warp, g/v, truncation,
+ * array-shape mismatch, trailing bytes (storage.py:431-483, 312-329). ecsr_b200_load
+ * parses the same way and then packs like ecsr_b200_pack (values in the blob's f32/f64). */
+typedef struct ecsr_blob_info {
+    int64_t num_rows;
+    int64_t num_cols;
+    int32_t nsets;
+    int32_t warp_size;
+    int32_t delta_bits;
+    int32_t value_bits;     /* precision tag of the header */
+    int32_t value_bytes;    /* 4 (f32) or 8 (f64) on the wire */
+    int64_t num_blocks;     /* over all sets */
+    int64_t stored_cols;
+    int64_t real_nnz;
+} ecsr_blob_info;
+
+int ecsr_b200_parse(const uint8_t* blob, int64_t len, ecsr_blob_info* info);
+int ecsr_b200_load(const uint8_t* blob, int64_t len, int32_t device_dtype, int32_t flags,
+                   ecsr_dev** out);
+
 int ecsr_b200_info(const ecsr_dev* dev, int64_t* num_rows, int64_t* num_cols, int32_t* nsets,
                    int32_t* warp_size, int32_t* delta_bits, int32_t* value_bits,
                    int32_t* device_dtype);

@@ -3,6 +3,8 @@
 Public API (names follow the reference `ecsr` package, pkg/src/ecsr/__init__.py):
 
     to_device(ec) -> DeviceMatrix          validate once + pack (libecsr_b200.so)
+    load_device(path | bytes)              .ecsr blob -> DeviceMatrix in one native call
+    parse_blob(path | bytes)               native host-only parse + shape check of a blob
     spmv(W, x) -> y                        y = W x on the GPU (fp16 in, fp32 accumulate)
     spmv_ec(ec, x)                         executor.spmv_ec-compatible convenience
     EcCsrMatrix / EcCsrSet, serialize, deserialize, storage_components,
@@ -32,6 +34,19 @@ def to_device(ec, device_dtype: str = "f16", force_generic: bool = False, device
     from .device import to_device as _to_device
 
     return _to_device(ec, device_dtype=device_dtype, force_generic=force_generic, device=device)
+
+
+def load_device(blob_or_path, device_dtype: str = "f16", force_generic: bool = False, device=None):
+    from .device import load_device as _load_device
+
+    return _load_device(blob_or_path, device_dtype=device_dtype, force_generic=force_generic,
+                        device=device)
+
+
+def parse_blob(blob_or_path) -> dict:
+    from .device import parse_blob as _parse_blob
+
+    return _parse_blob(blob_or_path)
 
 
 def spmv(W, x, y=None, accumulate: bool = False, ordered: bool = False, stream=None):

@@ -45,6 +45,15 @@ class SetInfo(ctypes.Structure):
                 ("stored_cols", c_i64), ("real_nnz", c_i64)]
 
 
+class BlobInfo(ctypes.Structure):
+    _fields_ = [("num_rows", c_i64), ("num_cols", c_i64), ("nsets", c_i32), ("warp_size", c_i32),
+                ("delta_bits", c_i32), ("value_bits", c_i32), ("value_bytes", c_i32),
+                ("num_blocks", c_i64), ("stored_cols", c_i64), ("real_nnz", c_i64)]
+
+    def to_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class Bytes(ctypes.Structure):
     _fields_ = [("row_indices", c_i64), ("block_indptr", c_i64), ("base_indices", c_i64),
                 ("delta_indices", c_i64), ("pad_mask", c_i64), ("block_values", c_i64),
@@ -62,6 +71,8 @@ SIGNATURES = {
     "ecsr_b200_pack": (c_i32, [ctypes.POINTER(HostSet), c_i32, c_i64, c_i64, c_i32, c_i32, c_i32,
                                c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "ecsr_b200_spmv": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "ecsr_b200_parse": (c_i32, [c_vp, c_i64, ctypes.POINTER(BlobInfo)]),
+    "ecsr_b200_load": (c_i32, [c_vp, c_i64, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "ecsr_b200_info": (c_i32, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
                                ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),

@@ -179,6 +179,10 @@ T* dalloc_copy(const std::vector<T>& h, int64_t* total, cudaError_t* err) {
 
 }  // namespace
 
+namespace ecsr_internal {  // other translation units (ecsr_loader.cpp) report errors here
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace ecsr_internal
+
 struct ecsr_dev {
     int device = 0;
     int64_t M = 0, K = 0;

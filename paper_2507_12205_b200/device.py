@@ -123,6 +123,45 @@ def to_device(ec, device_dtype: str = "f16", force_generic: bool = False,
     return DeviceMatrix(out.value, int(ec.num_rows), int(ec.num_cols), device_dtype, index)
 
 
+def _blob(blob_or_path):
+    if isinstance(blob_or_path, (bytes, bytearray, memoryview)):
+        return bytes(blob_or_path)
+    with open(blob_or_path, "rb") as fh:
+        return fh.read()
+
+
+def parse_blob(blob_or_path) -> dict:
+    """Host-only parse + shape check of a `.ecsr` blob by the native loader; raises
+    ContainerError with the reference's message on corruption (`storage.py:431-483`)."""
+    data = _blob(blob_or_path)
+    info = _lib.BlobInfo()
+    buf = ctypes.create_string_buffer(data, len(data))
+    _lib.check(_lib.lib().ecsr_b200_parse(buf, len(data), ctypes.byref(info)), "ecsr_b200_parse")
+    return info.to_dict()
+
+
+def load_device(blob_or_path, device_dtype: str = "f16", force_generic: bool = False,
+                device=None) -> DeviceMatrix:
+    """`.ecsr` blob (bytes or path) straight to a device handle: the native loader parses
+    the wire format and packs without building numpy sets (`load_container` + `to_device`
+    in one C call, same rejection rules)."""
+    torch = _torch()
+    if device_dtype not in _DEVICE_DTYPES:
+        raise ValueError(f"device_dtype must be one of {sorted(_DEVICE_DTYPES)}")
+    data = _blob(blob_or_path)
+    info = parse_blob(data)
+    dev = torch.device("cuda" if device is None else device)
+    index = dev.index if dev.index is not None else torch.cuda.current_device()
+    out = ctypes.c_void_p()
+    flags = _lib.PACK_FORCE_GENERIC if force_generic else _lib.PACK_DEFAULT
+    buf = ctypes.create_string_buffer(data, len(data))
+    with torch.cuda.device(index):
+        rc = _lib.lib().ecsr_b200_load(buf, len(data), _DEVICE_DTYPES[device_dtype], flags,
+                                       ctypes.byref(out))
+    _lib.check(rc, "ecsr_b200_load")
+    return DeviceMatrix(out.value, int(info["num_rows"]), int(info["num_cols"]), device_dtype, index)
+
+
 def spmv(W: DeviceMatrix, x, y=None, accumulate: bool = False, ordered: bool = False,
          stream=None):
     """y = W x (y += W x with accumulate). x: device tensor [K] of W.x_dtype.

@@ -5,4 +5,4 @@ name=$1; shift
 mkdir -p paper_2507_12205_b200/exp
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2,-fopenmp,-mpopcnt "$@" \
   -shared -o paper_2507_12205_b200/exp/lib$name.so paper_2507_12205_b200/csrc/ecsr_b200.cu \
-  paper_2507_12205_b200/csrc/ecsr_encoder.cpp -lgomp
+  paper_2507_12205_b200/csrc/ecsr_encoder.cpp paper_2507_12205_b200/csrc/ecsr_loader.cpp -lgomp
