@@ -10,6 +10,7 @@ Public API (names follow the reference `ecsr` package, pkg/src/ecsr/__init__.py)
     EcCsrMatrix / EcCsrSet, serialize, deserialize, storage_components,
     kernel_model_bytes, validate_container  host container (storage.py mirror)
     backend.register()                     plug into ecsr._kernels as backend "b200"
+    linear.SparseLinear                    torch.nn.Module for decode-time linear layers
 """
 
 from .container import (  # noqa: F401

@@ -108,6 +108,39 @@ def measure(label, kind, m, k, s, seed, shards):
             "sets": [(st.granularity, st.vector_size, st.num_blocks) for st in ec.sets]}
 
 
+def measure_sequence():
+    """Config 4 as a decoder-layer sequence: q|k|v row-stacked into
+    one launch sharing x, then o, fc1, fc2, PDL-chained in one CUDA graph; per-layer
+    time over a > L2 working set (one layer is ~590 MB)."""
+    from paper_2507_12205_b200.device import vstack
+
+    t0 = time.time()
+    mats = {}
+    for name, m, k, seed in (("q", 7168, 7168, 401), ("k", 7168, 7168, 404), ("v", 7168, 7168, 405),
+                             ("o", 7168, 7168, 406), ("fc1", 28672, 7168, 402), ("fc2", 7168, 28672, 403)):
+        mats[name] = convert_csr(make_matrix("magnitude", m, k, 0.7, seed, dtype=np.float32))
+    enc_s = time.time() - t0
+    launches = [("qkv", ["q", "k", "v"]), ("o", ["o"]), ("fc1", ["fc1"]), ("fc2", ["fc2"])]
+    ecs = {ln: vstack([mats[n] for n in names]) for ln, names in launches}
+    Ws = {ln: to_device(ec) for ln, ec in ecs.items()}
+    mb = sum(kernel_model_bytes(ec) for ec in ecs.values())
+    xs, ys, rel = {}, {}, 0.0
+    for i, (ln, _) in enumerate(launches):
+        x = np.random.default_rng(4000 + i).uniform(-1, 1, ecs[ln].num_cols).astype(np.float16)
+        xs[ln] = torch.from_numpy(x).cuda()
+        ys[ln] = torch.empty(ecs[ln].num_rows, device="cuda")
+        y = spmv(Ws[ln], xs[ln], y=ys[ln]).cpu().numpy()
+        ref = oracle.spmv_ec_oracle(ecs[ln].astype(np.float16).astype(np.float32), x.astype(np.float32),
+                                    np.float32)
+        rel = max(rel, float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30)))
+    layer_us = time_graph(lambda: [spmv(Ws[ln], xs[ln], y=ys[ln]) for ln, _ in launches], 50)
+    return {"matrix": "OPT30B decoder layer @70% (q|k|v, o, fc1, fc2 in one graph)", "model_bytes": mb,
+            "layer_us": round(layer_us, 2), "stream_us": round(layer_us, 2),
+            "stream_GBps": round(mb / layer_us / 1e3, 1), "stream_frac": round(mb / layer_us / 1e3 / PEAK, 3),
+            "target_us_70pct": round(mb / (0.7 * PEAK) / 1e3, 1), "parity_rel_inf": rel,
+            "encode_s": round(enc_s, 1), "launches": [ln for ln, _ in launches]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.jsonl"))
@@ -115,8 +148,11 @@ def main():
     args = ap.parse_args()
     with open(args.out, "w") as fh:
         for c in [int(v) for v in args.only.split(",")]:
-            for case in CONFIGS[c]:
-                r = measure(*case)
+            cases = [lambda case=case: measure(*case) for case in CONFIGS[c]]
+            if c == 4:
+                cases.append(measure_sequence)
+            for run in cases:
+                r = run()
                 r["config"] = c
                 line = json.dumps(r)
                 print(line, flush=True)

@@ -134,3 +134,4 @@ def test_load_device_matches_to_device(name):
         ya = spmv(a, x, ordered=True)
         yb = spmv(b, x, ordered=True)
         assert torch.equal(ya, yb)
+
