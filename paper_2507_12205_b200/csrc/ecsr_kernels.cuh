@@ -529,12 +529,13 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     __shared__ uint32_t rec_next;                   // dynamic record scheduler
     __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per ring stage
     // The stages form a pool, not an in-order ring: the producer refills whichever stage
-    // was released (a long record then holds one stage, not the whole ring). It tags a
-    // stage with (tile << 1 | parity of this fill of its full barrier) before the copy;
-    // consumers look their tile up by tag and wait on that parity.
-    __shared__ uint32_t stage_tile[kMaxRingStages];
+    // was released (a long record then holds one stage, not the whole ring). Before the
+    // copy it publishes (tile, stage, parity of this fill of the stage's full barrier) in
+    // the tile -> stage map; consumers look their tile up there and wait on that parity.
     __shared__ uint32_t tile_rec_s[kTileRecCache];
-    __shared__ uint32_t stage_free[kMaxRingStages];  // 1: the producer may refill this stage
+    // tile -> stage map (ring of 32 > kMaxRingStages tiles in flight): entry
+    // (tile << 6 | stage << 1 | parity), written by the producer at issue
+    __shared__ uint32_t tile_stage[32];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -547,9 +548,8 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         for (int s = 0; s < p.nstages; ++s) {
             mbar_init(&full[s], 1);
             stage_done[s] = 0;
-            stage_tile[s] = 0xffffffffu;
-            stage_free[s] = 1;
         }
+        for (int i = 0; i < 32; ++i) tile_stage[i] = 0xffffffffu;
         mbar_init(xbar, 1);
         rec_next = 0;
         gate_target = 0;
@@ -573,27 +573,45 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         const uint64_t policy = l2_evict_first_policy();
         uint32_t fill_parity = 0;  // bit s: parity of the next fill of stage s
         uint32_t t = t0;
+        // lane s < nstages: records of the tile in stage s (0 = empty). A stage is free
+        // once the consumers' done count (a shared red, no return value on their side)
+        // reaches it.
+        uint32_t expect = 0;
+        // record prefix counts of tiles [win_base, win_base + 32) in the lanes (one
+        // coalesced load per 31 tiles, no global round trip per issue)
+        uint32_t win_base = t0;
+        uint32_t win = t0 + lane <= t1 ? p.tile_rec[t0 + lane] : 0u;
         auto issue = [&]() {
             uint32_t freeset;
             while (true) {
                 uint32_t f = 0;
-                if (lane < p.nstages)
-                    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(f) : "r"(smem_addr(&stage_free[lane])) : "memory");
+                if (lane < p.nstages) {
+                    uint32_t done;
+                    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(done) : "r"(smem_addr(&stage_done[lane])) : "memory");
+                    f = done == expect;
+                }
                 freeset = __ballot_sync(0xffffffffu, f != 0);
                 if (freeset) break;
                 __nanosleep(20);
             }
             const int stage = __ffs(freeset) - 1;
+            if (t + 1 - win_base >= 32u) {  // warp-uniform window slide
+                win_base = t;
+                win = t + lane <= t1 ? p.tile_rec[t + lane] : 0u;
+            }
+            const uint32_t nrec = __shfl_sync(0xffffffffu, win, t + 1 - win_base) -
+                                  __shfl_sync(0xffffffffu, win, t - win_base);
+            if (lane == stage) expect = nrec;
             if (lane == 0) {
-                stage_free[stage] = 0;
+                stage_done[stage] = 0;
                 // generic-proxy reads of the old tile are complete (their values were
                 // consumed); order them before the async-proxy overwrite
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 const uint32_t par = (fill_parity >> stage) & 1u;
                 const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
                 const uint32_t bytes = (b - a) * 16u;
-                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_tile[stage])),
-                             "r"(((t - t0) << 1) | par)
+                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&tile_stage[(t - t0) & 31u])),
+                             "r"(((t - t0) << 6) | (static_cast<uint32_t>(stage) << 1) | par)
                              : "memory");
                 mbar_arrive_expect_tx(&full[stage], bytes);
                 bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a) * 16u, bytes,
@@ -684,14 +702,12 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         const unsigned long long c0 = clock64();
 #endif
         uint32_t stage, par;
-        while (true) {  // find the stage holding tile ti (lane s reads stage s's tag)
-            uint32_t tag = 0xffffffffu;
-            if (lane < p.nstages)
-                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(smem_addr(&stage_tile[lane])) : "memory");
-            const uint32_t hit = __ballot_sync(0xffffffffu, (tag >> 1) == ti);
-            if (hit) {
-                stage = __ffs(hit) - 1;
-                par = __shfl_sync(0xffffffffu, tag, stage) & 1u;
+        while (true) {  // the stage holding tile ti (tile -> stage map, one broadcast load)
+            uint32_t e;
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(e) : "r"(smem_addr(&tile_stage[ti & 31u])) : "memory");
+            if ((e >> 6) == ti) {
+                stage = (e >> 1) & 31u;
+                par = e & 1u;
                 break;
             }
             __nanosleep(64);
@@ -714,14 +730,9 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         ++nwork;
 #endif
         __syncwarp();
-        if (lane == 0) {
-            const uint32_t done = atomicAdd(&stage_done[stage], 1u) + 1u;
-            if (done == th[0]) {  // all records of this tile finished: release the stage
-                stage_done[stage] = 0;
-                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&stage_free[stage])), "r"(1u)
-                             : "memory");
-            }
-        }
+        if (lane == 0)  // record done (its stage reads were consumed by the FMAs above):
+                        // the producer refills the stage once all of its records are
+            asm volatile("red.relaxed.cta.shared.add.u32 [%0], 1;" ::"r"(smem_addr(&stage_done[stage])) : "memory");
     }
     ECSR_TRACE(4, threadIdx.x == 0);
     if (p.trace && lane == 0) {
