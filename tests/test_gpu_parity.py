@@ -256,3 +256,36 @@ def test_ring_wraps_many_times_small_tiles(tile, monkeypatch):
     out = subprocess.run([_sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_many_tiles_per_cta_wrap_stage_map():
+    # > 32 tiles per CTA: the producer's 32-tile record-count window slides and the
+    # 32-entry tile -> stage map wraps many times (tiny tiles, one record each)
+    import subprocess
+    import sys as _sys
+
+    code = (
+        "import numpy as np, torch, oracle;"
+        "from paper_2507_12205_b200.device import spmv, to_device;"
+        "from paper_2507_12205_b200.encoder import convert_csr;"
+        "from paper_2507_12205_b200.generators import make_matrix;"
+        "ec = convert_csr(make_matrix('magnitude', 4096, 4096, 0.5, 7, dtype=np.float32));"
+        "W = to_device(ec); b = W.bytes();"
+        "assert b['tiles'] > 32 * b['grid'], (b['tiles'], b['grid']);"
+        "x = np.random.default_rng(2).uniform(-1, 1, 4096);"
+        "xd = torch.from_numpy(x.astype(np.float16)).cuda();"
+        "ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),"
+        " x.astype(np.float16).astype(np.float32), np.float32);"
+        "y = spmv(W, xd, ordered=True).cpu().numpy(); assert np.array_equal(y, ref);"
+        "ys = [spmv(W, xd).cpu().numpy() for _ in range(5)];"
+        "assert all(np.max(np.abs(v - ref)) <= 1e-5 * np.max(np.abs(ref)) for v in ys);"
+        "print('ok')"
+    )
+    import os as _os
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    env = dict(_os.environ, ECSR_B200_TILE="1024",
+               PYTHONPATH=_os.pathsep.join([root, _os.path.join(root, "tests")]))
+    out = subprocess.run([_sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
