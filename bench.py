@@ -552,10 +552,36 @@ def run_ours(args):
     h2d = sum(x.numel() * 2 for x in xs_host.values())
     d2h = sum(y.numel() * 4 for y in ys_host.values())
 
+    # The first launch's x and the last launch's y are on the critical path; the other
+    # inputs go up, and the other outputs come back, on a side stream while launches run.
+    side = torch.cuda.Stream(dev)
+    k0 = kdim[LAUNCHES[0][0]]
+    m_last = handles[LAUNCHES[-1][0]].num_rows
+
     def e2e_body():
-        x_all.copy_(x_host_all, non_blocking=True)
-        step()
-        y_host_all.copy_(y_all, non_blocking=True)
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        side.wait_event(fork)
+        x_all[:k0].copy_(x_host_all[:k0], non_blocking=True)
+        with torch.cuda.stream(side):
+            x_all[k0:].copy_(x_host_all[k0:], non_blocking=True)
+            x_rest = torch.cuda.Event()
+            x_rest.record(side)
+        ev = {}
+        for i, (ln, _) in enumerate(LAUNCHES):
+            if i == 1:
+                stream.wait_event(x_rest)
+            spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
+            if i == len(LAUNCHES) - 2:
+                ev["head_done"] = torch.cuda.Event()
+                ev["head_done"].record(stream)
+        with torch.cuda.stream(side):
+            side.wait_event(ev["head_done"])
+            y_host_all[:-m_last].copy_(y_all[:-m_last], non_blocking=True)
+            y_head = torch.cuda.Event()
+            y_head.record(side)
+        y_host_all[-m_last:].copy_(y_all[-m_last:], non_blocking=True)
+        stream.wait_event(y_head)  # join
 
     # the same step with its host<->device copies, captured once (pinned-host memcpy
     # nodes + the 4 launches) so the host API overhead does not dominate 100 us steps
