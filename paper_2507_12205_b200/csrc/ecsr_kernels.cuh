@@ -2,15 +2,17 @@
 //
 // Two kernels compute y = A x over an EC-CSR container (pkg/src/ecsr/storage.py:50-96):
 //
-//  * ecsr_tiled_kernel -- the product. Persistent grid (one CTA per SM). The packer
-//    lays every block out block-major in one arena, grouped into <= ~8 KB tiles of
-//    whole blocks; each CTA owns a contiguous, byte-balanced tile range. One producer
-//    thread streams tiles HBM -> shared memory with cp.async.bulk (TMA bulk copies,
-//    SASS UBLKCP) into an mbarrier-guarded ring; NCONS consumer warps stage x (fp16)
-//    in shared memory once, then each decodes whole blocks: per-lane delta decode in
-//    registers, x gathered from shared memory, g FP32 FMAs per column, butterfly
-//    reduce-scatter over lanes, then red.global.add.f32 into y (or one partial per
-//    block row for the ordered, bitwise-reproducible mode).
+//  * ecsr_tiled_kernel -- the product. Persistent grid: two co-resident CTAs per SM
+//    (8 consumer warps each) while x fits twice, else one (16 consumer warps). The
+//    packer lays the container out as group records (P blocks of one set whose chunk
+//    streams are interleaved: P*g row accumulators per warp) packed into tiles that
+//    fill the CTA's stage pool; each CTA owns a contiguous, cost-balanced tile range.
+//    A producer warp streams tiles HBM -> shared memory with cp.async.bulk (TMA bulk
+//    copies, SASS UBLKCP) into an mbarrier-guarded stage pool; consumer warps take
+//    records from a shared counter: per-lane delta decode (IDP.4A), x (fp16) gathered
+//    from shared memory, FHFMA (f16 x f16 + f32), butterfly reduce-scatter over lanes,
+//    then red.global.add.f32 into y (or one partial per block row for the ordered,
+//    bitwise-reproducible mode).
 //
 //  * ecsr_generic_kernel -- the reference's arithmetic for ANY container
 //    (W <= 32, any v, g, B in {4, 8, 16}; f16/f32/f64), one warp per block straight
@@ -502,13 +504,13 @@ __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P
     }
 }
 
-// Persistent grid, one CTA per SM, warp-specialised:
-//   * producer warp (one elected lane): streams this CTA's byte-balanced tile range
-//     HBM -> shared memory with cp.async.bulk into an mbarrier ring, L2 evict_first;
-//     it starts before griddepcontrol.wait because the weights never depend on the
-//     previous kernel (PDL overlap of weight streaming with the predecessor's tail);
-//   * consumer warps: wait for the predecessor (x producer), stage x (fp16) in shared
-//     memory, then decode blocks from the ring.
+// Persistent grid (1 or 2 CTAs per SM, kConsumerWarpsPerSm above), warp-specialised:
+//   * producer warp: streams this CTA's tile range HBM -> shared memory with
+//     cp.async.bulk into the stage pool, L2 evict_first; the first tiles go out before
+//     griddepcontrol.wait because the weights never depend on the previous kernel (PDL
+//     overlap of weight streaming with the predecessor's tail);
+//   * consumer warps: wait for the predecessor (x producer) and for x in shared
+//     memory, then decode records from the pool.
 // Overwrite without a memset launch (zero_y): every CTA zeroes its slice of y, then
 // bumps a 64-bit generation counter; warps pass the gate (counter reached the
 // generation's multiple of gridDim.x) before their first red.global. PDL dependents
