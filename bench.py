@@ -308,6 +308,11 @@ def run_sharded(args):
     os.environ.setdefault("WORLD_SIZE", str(world))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    # NCCL / c10d print banners on fd 1 when communicators come up: route fd 1 to stderr
+    # for the run and write rank 0's one JSON line to the saved stdout
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     dist.init_process_group("nccl", device_id=dev)
     ecs, bounds = load_shards(rank, world)
     local_bytes = sum(kernel_model_bytes(ec) for ec in ecs.values())
@@ -409,9 +414,36 @@ def run_sharded(args):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms, e2e_ms], device=dev)
+    # the step's two halves timed apart (SURVEY.md §8(e) reporting): the per-GPU shard
+    # SpMVs alone and the y all-gathers alone, each as its own graph when capturable
+    def split_ms(body):
+        try:
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=stream):
+                body()
+            run = g2.replay
+        except Exception:  # noqa: BLE001
+            torch.cuda.synchronize()
+            run = body
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                run()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    spmv_ms = split_ms(lambda: [spmv(handles[ln], xs[ln], y=ypad[ln][:handles[ln].num_rows], stream=stream)
+                                for ln, _ in LAUNCHES])
+    gather_ms = split_ms(lambda: [dist.all_gather_into_tensor(yall[ln], ypad[ln]) for ln, _ in LAUNCHES])
+    t = torch.tensor([ms, e2e_ms, spmv_ms, gather_ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, e2e_ms = t.tolist()
+    ms, e2e_ms, spmv_ms, gather_ms = t.tolist()
     if rank == 0:
         peak, peak_kind = peaks()
         h2d = sum(x.numel() * 2 for x in xs_host.values())
@@ -436,8 +468,12 @@ def run_sharded(args):
                          "traffic": None, "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel"},
             "gpu_launches": len(LAUNCHES) * args.steps,
             "clocks": clocks.summary(),
+            "sharded": {"spmv_ms_per_step": round(spmv_ms, 5), "allgather_ms_per_step": round(gather_ms, 5),
+                        "step_ms": round(ms, 5), "allgather_bytes_per_rank_per_step":
+                        sum(int(ypad[ln].numel()) * 4 for ln in ypad)},
         }
-        print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.destroy_process_group()
 
 
