@@ -259,9 +259,11 @@ def test_ring_wraps_many_times_small_tiles(tile, monkeypatch):
 
 
 @pytest.mark.gpu
-def test_many_tiles_per_cta_wrap_stage_map():
+@pytest.mark.parametrize("rows,sparsity,per_cta", [(4096, 0.5, 32), (114688, 0.95, 256)])
+def test_many_tiles_per_cta_wrap_stage_map(rows, sparsity, per_cta):
     # > 32 tiles per CTA: the producer's 32-tile record-count window slides and the
-    # 32-entry tile -> stage map wraps many times (tiny tiles, one record each)
+    # 32-entry tile -> stage map wraps many times (tiny tiles, one record each); > 256:
+    # the consumers' shared prefix-count cache overflows to global loads
     import subprocess
     import sys as _sys
 
@@ -270,9 +272,9 @@ def test_many_tiles_per_cta_wrap_stage_map():
         "from paper_2507_12205_b200.device import spmv, to_device;"
         "from paper_2507_12205_b200.encoder import convert_csr;"
         "from paper_2507_12205_b200.generators import make_matrix;"
-        "ec = convert_csr(make_matrix('magnitude', 4096, 4096, 0.5, 7, dtype=np.float32));"
+        f"ec = convert_csr(make_matrix('magnitude', {rows}, 4096, {sparsity}, 7, dtype=np.float32));"
         "W = to_device(ec); b = W.bytes();"
-        "assert b['tiles'] > 32 * b['grid'], (b['tiles'], b['grid']);"
+        f"assert b['tiles'] > {per_cta} * b['grid'], (b['tiles'], b['grid']);"
         "x = np.random.default_rng(2).uniform(-1, 1, 4096);"
         "xd = torch.from_numpy(x.astype(np.float16)).cuda();"
         "ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),"
