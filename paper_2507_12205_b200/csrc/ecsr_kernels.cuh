@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     uint32_t tile_end = tile_rec_at(1);
     uint32_t tile_begin = 0;
 #ifdef ECSR_TRACE_CYCLES
-    unsigned long long cyc_wait = 0, cyc_work = 0, nwork = 0;
+    unsigned long long cyc_wait = 0, cyc_work = 0, nwork = 0, cyc_unissued = 0;
 #endif
     while (true) {
         uint32_t k = 0;
@@ -714,6 +714,9 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             }
             __nanosleep(64);
         }
+#ifdef ECSR_TRACE_CYCLES
+        cyc_unissued += clock64() - c0;  // the tile was not issued yet (no free stage)
+#endif
         mbar_wait(&full[stage], par);
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c1 = clock64();
@@ -744,6 +747,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         atomicAdd(p.trace + blockIdx.x * 16 + 8, cyc_wait);
         atomicAdd(p.trace + blockIdx.x * 16 + 9, cyc_work);
         atomicAdd(p.trace + blockIdx.x * 16 + 10, nwork);
+        atomicAdd(p.trace + blockIdx.x * 16 + 13, cyc_unissued);
 #endif
         atomicAdd(p.trace + blockIdx.x * 16 + 11, static_cast<unsigned long long>(t1 - t0));
     }

@@ -47,4 +47,5 @@ print("corr(end, ntiles) =", float(np.corrcoef(end, nt)[0, 1]))
 if t[:, 10].sum() > 0:  # ECSR_TRACE_CYCLES build: consumer wait vs work cycles
     wait, work, nrec = t[:, 8].sum(), t[:, 9].sum(), t[:, 10].sum()
     print(f"consumer cycles: wait {wait / (wait + work):.1%} of wait+work; "
-          f"work per record {work / nrec:.0f}, wait per record {wait / nrec:.0f} cycles; records {nrec}")
+          f"work per record {work / nrec:.0f}, wait per record {wait / nrec:.0f} cycles "
+          f"(tile not yet issued: {t[:, 13].sum() / nrec:.0f}); records {nrec}")
