@@ -669,11 +669,15 @@ def run_ours(args):
     # launch duration over the timed region is ms / launches and the algorithmic bytes of
     # a launch average step_bytes / launches
     achieved = step_bytes / (ms * 1e-3) / 1e9
+    # traffic: ncu dram__bytes_read + write of the kernel, per launch like `achieved`
+    # (the committed capture's per-step total over the step's launches)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_step")
+            per_step = json.load(fh).get("dram_bytes_per_step")
+        if per_step:
+            traffic = round(per_step / len(LAUNCHES))
     line = {
         "metric": METRIC,
         "value": round(world * step_bytes / (ms * 1e-3) / 1e9, 1), "unit": "GB/s",
@@ -692,6 +696,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": round(step_bytes / len(LAUNCHES)),
                      "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel",
                      "device_arena_bytes": {ln: layout[ln]["device_arena_bytes"] for ln in layout}},
         "gpu_launches": len(LAUNCHES) * args.steps,
