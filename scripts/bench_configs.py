@@ -6,7 +6,9 @@ Inputs: seeded synthetic matrices (magnitude-pruned N(0, 1/K) or planted blocks)
 encoded by the native encoder (byte-identical to the reference convert_csr). For each
 matrix: `stream_us` = average device time per SpMV when launched back to back (CUDA
 graph over rotating copies whose total exceeds 2x L2, as in a layer sequence),
-`single_us` = one launch after a 256 MB L2 flush, GB/s = model bytes / time, frac vs
+`single_us` = one launch after a 256 MB L2 flush, GB/s = model bytes / time (stream:
+mean of 40 back-to-back graph replays; p10/p50/p90 from a second pass with an event
+between replays, which costs them their overlap), frac vs
 the 6.65 TB/s fallback HBM peak. Parity: fast-mode y vs the C oracle on fp16-rounded
 inputs (rel-inf). Config 5 reports the per-GPU shard SpMV of an N-way row split
 (the NCCL all-gather needs more than the one GPU available here).
@@ -66,7 +68,16 @@ def time_graph(fn, reps):
         for _ in range(reps):
             g.replay()
         e1.record(s)
+        # per-replay spread from a second pass with an event between replays (the events
+        # cost the replays their back-to-back overlap, so the mean comes from the first)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        ev[0].record(s)
+        for i in range(reps):
+            g.replay()
+            ev[i + 1].record(s)
     torch.cuda.synchronize()
+    per = np.array([ev[i].elapsed_time(ev[i + 1]) * 1e3 for i in range(reps)])
+    time_graph.spread = (float(np.percentile(per, 10)), float(np.median(per)), float(np.percentile(per, 90)))
     return e0.elapsed_time(e1) * 1e3 / reps
 
 
@@ -87,7 +98,8 @@ def measure(label, kind, m, k, s, seed, shards):
     y = spmv(Ws[0], xd, y=ys[0]).cpu().numpy()
     ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32), x.astype(np.float32), np.float32)
     rel = float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
-    stream_us = time_graph(lambda: [spmv(Ws[i], xd, y=ys[i]) for i in range(ncopy)], 20) / ncopy
+    stream_us = time_graph(lambda: [spmv(Ws[i], xd, y=ys[i]) for i in range(ncopy)], 40) / ncopy
+    p10, p50, p90 = (v / ncopy for v in time_graph.spread)
     flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
     singles = []
     for _ in range(10):
@@ -101,7 +113,8 @@ def measure(label, kind, m, k, s, seed, shards):
     single_us = float(np.median(singles))
     return {"matrix": label, "rows": ec.num_rows, "cols": k, "nnz": ec.nnz,
             "shards": shards, "model_bytes": mb, "layout": Ws[0].layout,
-            "stream_us": round(stream_us, 2), "stream_GBps": round(mb / stream_us / 1e3, 1),
+            "stream_us": round(stream_us, 2), "stream_us_p10_p50_p90": [round(p10, 2), round(p50, 2), round(p90, 2)],
+            "stream_GBps": round(mb / stream_us / 1e3, 1),
             "stream_frac": round(mb / stream_us / 1e3 / PEAK, 3),
             "single_us": round(single_us, 2), "single_GBps": round(mb / single_us / 1e3, 1),
             "parity_rel_inf": rel, "encode_s": round(enc_s, 1),
@@ -133,9 +146,10 @@ def measure_sequence():
         ref = oracle.spmv_ec_oracle(ecs[ln].astype(np.float16).astype(np.float32), x.astype(np.float32),
                                     np.float32)
         rel = max(rel, float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30)))
-    layer_us = time_graph(lambda: [spmv(Ws[ln], xs[ln], y=ys[ln]) for ln, _ in launches], 50)
+    layer_us = time_graph(lambda: [spmv(Ws[ln], xs[ln], y=ys[ln]) for ln, _ in launches], 200)
     return {"matrix": "OPT30B decoder layer @70% (q|k|v, o, fc1, fc2 in one graph)", "model_bytes": mb,
             "layer_us": round(layer_us, 2), "stream_us": round(layer_us, 2),
+            "stream_us_p10_p50_p90": [round(v, 2) for v in time_graph.spread],
             "stream_GBps": round(mb / layer_us / 1e3, 1), "stream_frac": round(mb / layer_us / 1e3 / PEAK, 3),
             "target_us_70pct": round(mb / (0.7 * PEAK) / 1e3, 1), "parity_rel_inf": rel,
             "encode_s": round(enc_s, 1), "launches": [ln for ln, _ in launches]}
