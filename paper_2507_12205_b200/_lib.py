@@ -15,8 +15,7 @@ import numpy as np
 from .errors import ContainerError, DeviceError, EcsrError
 
 LIB_NAME = "libecsr_b200.so"
-LIB_PATH = os.environ.get("ECSR_B200_LIB") or os.path.join(
-    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)  # override: tuning builds only
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 OK, ERR_CONTAINER, ERR_VALUE, ERR_CUDA = 0, 1, 2, 3
 F16, F32, F64 = 1, 2, 3

@@ -13,7 +13,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .container import EcCsrMatrix, EcCsrSet
+from .container import EcCsrMatrix, EcCsrSet, check_set_shapes
 
 _DEVICE_DTYPES = {"f16": _lib.F16, "f32": _lib.F32, "f64": _lib.F64}
 
@@ -24,7 +24,7 @@ def _torch():
     return torch
 
 
-def _host_sets(ec):
+def _host_sets(ec, check_shapes: bool = True):
     """Coerce a container's sets to the C-ABI dtypes (copies only on mismatch, like
     np.ascontiguousarray in `_speedups.pyx:62-77`). Returns (HostSet array, keepalive)."""
     dtype = np.dtype(ec.dtype)
@@ -32,6 +32,10 @@ def _host_sets(ec):
         raise ValueError("container values must be float32 or float64")
     keep = []
     arr = (_lib.HostSet * max(len(ec.sets), 1))()
+    for s in ec.sets if check_shapes else ():
+        # array lengths against the declared sizes BEFORE any pointer crosses the C-ABI
+        # (storage.py:312-329): the native validator trusts num_blocks / stored_cols
+        check_set_shapes(s, int(ec.warp_size))
     for i, s in enumerate(ec.sets):
         rows = np.ascontiguousarray(s.row_indices, dtype=np.uint32)
         indptr = np.ascontiguousarray(s.block_indptr, dtype=np.int64)

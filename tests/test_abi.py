@@ -59,11 +59,24 @@ def test_to_f16_matches_numpy_rne():
     assert np.isnan(got.view(np.float16)[0])
 
 
-def _host_set(ec, i=0):
+def _host_set(ec, check_shapes=True):
     from paper_2507_12205_b200.device import _host_sets
 
-    arr, keep, dt = _host_sets(ec)
+    arr, keep, dt = _host_sets(ec, check_shapes)
     return arr, keep, dt
+
+
+def test_short_arrays_rejected_before_the_c_abi():
+    """Arrays shorter than the declared sizes never reach the native validator (which
+    would read past them): ContainerError like the reference's _check_set_shapes."""
+    from conftest import load_golden
+
+    from paper_2507_12205_b200.errors import ContainerError
+
+    ec = load_golden("uniform_256x256_s0.5_b8_seed11")["ec"]
+    ec.sets[0].delta_indices = ec.sets[0].delta_indices[:-128]
+    with pytest.raises(ContainerError, match="length mismatch"):
+        _host_set(ec)
 
 
 @pytest.mark.parametrize("corrupt,code", [
@@ -76,10 +89,14 @@ def test_pack_validation_errors_need_no_gpu(corrupt, code):
     ec = load_golden("uniform_256x256_s0.5_b8_seed11")["ec"]
     s = ec.sets[0]
     warp = ec.warp_size
-    if corrupt == "indptr":
+    if corrupt == "indptr":  # last block 64 columns wider: not a multiple of W*v = 128
         s.block_indptr = s.block_indptr.copy()
-        s.block_indptr[-1] += 128
-        s.stored_cols += 128
+        s.block_indptr[-1] += 64
+        s.stored_cols += 64
+        s.delta_indices = np.concatenate([s.delta_indices, np.zeros(64, s.delta_indices.dtype)])
+        s.pad_mask = np.concatenate([s.pad_mask, np.ones(64, np.bool_)])
+        s.block_values = np.concatenate([s.block_values,
+                                         np.zeros(64 * s.granularity, s.block_values.dtype)])
     elif corrupt == "delta":
         s.delta_indices = s.delta_indices.copy()
         s.delta_indices[3] = 256
@@ -92,7 +109,8 @@ def test_pack_validation_errors_need_no_gpu(corrupt, code):
         s.row_indices[0] = ec.num_rows
     elif corrupt == "warp":
         warp = 33
-    arr, keep, dt = _host_set(ec)
+    # the native validator on its own (array lengths are consistent; contents are not)
+    arr, keep, dt = _host_set(ec, check_shapes=False)
     out = ctypes.c_void_p()
     rc = _lib.lib().ecsr_b200_pack(arr, len(ec.sets), ec.num_rows, ec.num_cols, warp,
                                    ec.delta_bits, 16, _lib.dtype_code(dt), _lib.F16, 0,
