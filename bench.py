@@ -1,12 +1,18 @@
 #!/usr/bin/env python
 """bench.py -- EC-CSR batch-1 SpMV hot path on B200 (BASELINE.json configs[1]).
 
-Workload ("llama7b-layer-s0.5"): the seven SpMVs of one LLaMA-7B decoder layer at 50 %
-per-row magnitude pruning (random N(0, 1/K) weights, seeded), encoded to EC-CSR by the
-reference pipeline (W=32, V=4, B=8; `convert_csr`, cached as .ecsr under cache/):
+Headline workload ("llama7b-layer-s0.5", configs[1]): the seven SpMVs of one LLaMA-7B
+decoder layer at 50 % per-row magnitude pruning (random N(0, 1/K) weights, seeded),
+EC-CSR-encoded with W=32, V=4, B=8 (`storage.convert_csr`, storage.py:700-708):
 q, k, v, o 4096x4096, gate, up 11008x4096, down 4096x11008. One step = the layer's
 SpMVs as 4 stream-ordered launches (q|k|v and gate|up row-stacked, because they share
 x; o; down), each y = W x with fp16 values and x, fp32 accumulate and y.
+
+Encodings: every container is sha256-checked against the REFERENCE encoder's output
+(tests/golden/ref_hashes.json, made by scripts/ref_hashes.py with the reference's own
+convert_csr). Inputs come from cache/*.ecsr when present (the reference arm writes
+them with the reference pipeline), else from the native encoder (byte-identical; the
+hash check proves it on every run).
 
 Reported (one JSON line, rank 0):
   value        algorithmic GB/s = model bytes per step / device time per step, with
@@ -18,17 +24,27 @@ Reported (one JSON line, rank 0):
   roofline     the tiled kernel's per-launch algorithmic bytes / its CUDA-event time,
                against the measured HBM copy peak (MEASURED_PEAKS.json, else the
                6.65 TB/s fallback of /opt/skills/guides/B200_PROFILING.md).
-  cpu_baseline the reference's own compiled kernel (oracle/_ref/_speedups*.so, built from
-               the reference's _speedups.pyx) driven like executor.spmv_ec, one core, on a
+  parity       every timed launch checked before timing: ordered mode bitwise equal to
+               the oracle (the reference kernel's arithmetic on fp16-rounded inputs),
+               fast mode rel-inf <= 1e-5 of it and rel-L2 <= 1e-3 of the FP32 result.
+  configs      the other BASELINE configs timed the same way: the OPT-30B decoder layer
+               @70 % (configs[3], the largest single-GPU config) and the single
+               4096x4096 @50 % SpMV of configs[0] (latency in us).
+  cpu_baseline the reference's own compiled kernel (oracle/_ref, built from the
+               reference's _speedups.pyx) driven like executor.spmv_ec, one core, on a
                bounded sample of the same workload.
 
-`--impl reference` runs only the reference CPU path (all host cores: one process per
-matrix of the layer) on the same workload and prints its line with "impl": "reference".
+`--impl reference` runs the UNMODIFIED reference package (baseline/_ref: `ecsr`, its
+compiled backend) on the same workload: encodes with the reference's convert_csr
+(parallel processes, one matrix each, cached in cache/), then times the stock
+single-process `executor.spmv_ec(ec, x, validate=False)` (executor.py:80-96) over the
+layer. libecsr_b200.so is never loaded on that path (checked from /proc/self/maps).
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -42,53 +58,99 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-WORKLOAD = "llama7b-layer-s0.5"
-# (name, generator, rows, cols, sparsity, seed, input)
-MATRICES = [
-    ("q", "magnitude", 4096, 4096, 0.5, 101, "x_attn"),
-    ("k", "magnitude", 4096, 4096, 0.5, 102, "x_attn"),
-    ("v", "magnitude", 4096, 4096, 0.5, 103, "x_attn"),
-    ("o", "magnitude", 4096, 4096, 0.5, 104, "x_o"),
-    ("gate", "magnitude", 11008, 4096, 0.5, 105, "x_mlp"),
-    ("up", "magnitude", 11008, 4096, 0.5, 106, "x_mlp"),
-    ("down", "magnitude", 4096, 11008, 0.5, 107, "x_down"),
-]
-# launches per step: matrices sharing an input are row-stacked into one container
-LAUNCHES = [("qkv", ["q", "k", "v"]), ("o", ["o"]), ("gate_up", ["gate", "up"]), ("down", ["down"])]
+REF_SRC = os.path.join(ROOT, "baseline", "_ref", "pkg", "src")
 FALLBACK_HBM_GBS = 6650.0
 METRIC = "SpMV latency (µs) and achieved HBM GB/s vs B200 roofline; speedup vs CPU ref"
+HEADLINE = "llama7b-layer-s0.5"
+
+# name -> matrices (name, generator, rows, cols, sparsity, seed) and launches (matrices
+# sharing x are row-stacked into one container)
+WORKLOADS = {
+    "llama7b-layer-s0.5": {
+        "desc": "LLaMA-7B decoder layer @50 % (BASELINE configs[1])",
+        "matrices": [
+            ("q", "magnitude", 4096, 4096, 0.5, 101), ("k", "magnitude", 4096, 4096, 0.5, 102),
+            ("v", "magnitude", 4096, 4096, 0.5, 103), ("o", "magnitude", 4096, 4096, 0.5, 104),
+            ("gate", "magnitude", 11008, 4096, 0.5, 105), ("up", "magnitude", 11008, 4096, 0.5, 106),
+            ("down", "magnitude", 4096, 11008, 0.5, 107),
+        ],
+        "launches": [("qkv", ["q", "k", "v"]), ("o", ["o"]), ("gate_up", ["gate", "up"]),
+                     ("down", ["down"])],
+    },
+    "opt30b-layer-s0.7": {
+        "desc": "OPT-30B decoder layer @70 % (BASELINE configs[3])",
+        "matrices": [
+            ("q", "magnitude", 7168, 7168, 0.7, 401), ("k", "magnitude", 7168, 7168, 0.7, 402),
+            ("v", "magnitude", 7168, 7168, 0.7, 403), ("o", "magnitude", 7168, 7168, 0.7, 404),
+            ("fc1", "magnitude", 28672, 7168, 0.7, 405), ("fc2", "magnitude", 7168, 28672, 0.7, 406),
+        ],
+        "launches": [("qkv", ["q", "k", "v"]), ("o", ["o"]), ("fc1", ["fc1"]), ("fc2", ["fc2"])],
+    },
+    "single-4096x4096-s0.5": {
+        "desc": "single 4096x4096 @50 % SpMV (BASELINE configs[0])",
+        "matrices": [("w", "magnitude", 4096, 4096, 0.5, 1)],
+        "launches": [("w", ["w"])],
+    },
+}
 
 
-def cache_path(name):
-    m = {n: (g, r, c, s, sd) for n, g, r, c, s, sd, _ in MATRICES}[name]
-    g, r, c, s, sd = m
-    return os.path.join(ROOT, "cache", f"{g}_{r}x{c}_s{s}_seed{sd}.ecsr")
+# the headline workload's tables (scripts/ use these)
+MATRICES = WORKLOADS[HEADLINE]["matrices"]
+LAUNCHES = WORKLOADS[HEADLINE]["launches"]
 
 
-def load_workload():
-    """EC-CSR encodings of the layer: cache/*.ecsr when present (scripts/make_cache.sh:
-    the reference's convert_csr), else the native encoder, which is byte-identical to
-    the reference (tests/test_encoder.py), writing the cache for the next run."""
-    from paper_2507_12205_b200.container import load_container, save_container
-    from paper_2507_12205_b200.encoder import convert_csr
-    from paper_2507_12205_b200.generators import make_matrix
+def workload_config(name, step_bytes):
+    """The `config` object; identical in both arms (the driver compares them)."""
+    w = WORKLOADS[name]
+    return {"workload": name, "matrices": [list(m) for m in w["matrices"]],
+            "launches_per_step": [ln for ln, _ in w["launches"]],
+            "model_bytes_per_step": int(step_bytes),
+            "l2": "inputs > 126 MB L2 per step (no flush)" if step_bytes > 126e6
+                  else "single SpMV: L2 flushed by streaming 512 MB between replays",
+            "encoder": "convert_csr W=32 V=4 B=8, sha256-equal to the reference encoding",
+            "x": "U(-1,1) fp16, numpy default_rng(5000), one draw per launch"}
 
-    ecs, sources = {}, set()
-    for name, kind, rows, cols, s, seed, _ in MATRICES:
-        path = cache_path(name)
-        if os.path.exists(path):
-            ecs[name] = load_container(path)
-            sources.add("cache")
-            continue
-        ecs[name] = convert_csr(make_matrix(kind, rows, cols, s, seed, dtype=np.float32))
-        sources.add("native-encoder")
-        try:
-            os.makedirs(os.path.dirname(path), exist_ok=True)
-            save_container(ecs[name], path + ".tmp")
-            os.replace(path + ".tmp", path)
-        except OSError:
-            pass
-    return ecs, sorted(sources)
+
+def launch_inputs(name):
+    """x of each launch (fp16), identical in both arms."""
+    w = WORKLOADS[name]
+    dims = {m[0]: m[3] for m in w["matrices"]}
+    rng = np.random.default_rng(5000)
+    return {ln: rng.uniform(-1, 1, dims[names[0]]).astype(np.float16) for ln, names in w["launches"]}
+
+
+def matrix_key(m):
+    _, kind, rows, cols, s, seed = m
+    return f"{kind}_{rows}x{cols}_s{s}_seed{seed}"
+
+
+def cache_path(m):
+    return os.path.join(ROOT, "cache", matrix_key(m) + ".ecsr")
+
+
+def ref_hashes():
+    path = os.path.join(ROOT, "tests", "golden", "ref_hashes.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+def sha256(data: bytes) -> str:
+    return hashlib.sha256(data).hexdigest()
+
+
+def model_bytes(ec) -> int:
+    """storage_report(ec, value_bits=16) components minus pad_mask and desc
+    (storage.py:592-613) + 2K (x fp16) + 4M (y fp32); duck-typed over the reference's
+    and this package's EcCsrMatrix."""
+    total = 0
+    for s in ec.sets:
+        total += 4 * s.num_blocks * s.granularity + 8 * (s.num_blocks + 1)
+        total += 4 * s.num_blocks * ec.warp_size + (s.stored_cols * ec.delta_bits + 7) // 8
+        total += s.stored_cols * s.granularity * 2
+    return total + 2 * ec.num_cols + 4 * ec.num_rows
 
 
 def peaks():
@@ -102,6 +164,21 @@ def peaks():
     except (OSError, ValueError):
         pass
     return FALLBACK_HBM_GBS, "fallback"
+
+
+def loaded_native_libs():
+    """Shared objects of this repo / the reference mapped into this process."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                path = line.split()[-1] if line.strip() else ""
+                if path.endswith(".so") or ".so." in path or ".cpython-" in path:
+                    if path.startswith(ROOT) or "_speedups" in path or "ecsr" in path:
+                        libs.add(os.path.relpath(path, ROOT) if path.startswith(ROOT) else path)
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 class ClockSampler:
@@ -164,38 +241,373 @@ def dist_env():
         os.environ.get("WORLD_SIZE", 1))
 
 
-def model_bytes(ecs):
-    from paper_2507_12205_b200.container import kernel_model_bytes
+# ------------------------------------------------------------------------------------
+# Reference arm: the unmodified reference package (baseline/_ref), no code of ours
+# ------------------------------------------------------------------------------------
 
-    return {n: kernel_model_bytes(ec) for n, ec in ecs.items()}
+def _import_reference():
+    if os.path.isdir(REF_SRC) and REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import ecsr  # noqa: F401
+    from ecsr import _kernels, executor, storage
+
+    return _kernels, executor, storage
+
+
+def _ref_encode_worker(m, path):
+    """One matrix through the reference's own pipeline (storage.convert_csr with the
+    default ExtractionConfig: W=32, V=4, B=8), serialized to `path`."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    _, _, storage = _import_reference()
+    from ecsr import core
+    from ecsr.extraction import ExtractionConfig
+
+    from paper_2507_12205_b200.generators import make_matrix  # numpy-only synthetic input
+
+    _, kind, rows, cols, s, seed = m
+    a = make_matrix(kind, rows, cols, s, seed, dtype=np.float32)
+    t0 = time.perf_counter()
+    ec = storage.convert_csr(core.CsrMatrix(a.num_rows, a.num_cols, a.row_ptr, a.col_idx, a.values),
+                             ExtractionConfig())
+    dt = time.perf_counter() - t0
+    blob = storage.serialize(ec)
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path + f".tmp{os.getpid()}", "wb") as fh:
+        fh.write(blob)
+    os.replace(path + f".tmp{os.getpid()}", path)
+    return dt
+
+
+def _ref_spmv_worker(m, set_ids, x, reps):
+    """Secondary all-cores figure: a subset of one matrix's block sets (their y
+    contributions add up), stock executor loop over that subset."""
+    _kernels, executor, storage = _import_reference()
+    with open(cache_path(m), "rb") as fh:
+        ec = storage.deserialize(fh.read())
+    sub = storage.EcCsrMatrix(ec.num_rows, ec.num_cols, ec.value_bits, ec.delta_bits, ec.warp_size,
+                              [ec.sets[i] for i in set_ids])
+    executor.spmv_ec(sub, x, validate=False)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        y = executor.spmv_ec(sub, x, validate=False)
+    return (time.perf_counter() - t0) / reps, y
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    try:
+        _kernels, executor, storage = _import_reference()
+    except ImportError as exc:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference package not importable: {exc}"}))
+        return
+    backend = _kernels.active_backend()
+    wl = WORKLOADS[HEADLINE]
+    hashes = ref_hashes()
+    # 1. encodings: the reference pipeline, one process per missing matrix
+    todo = [m for m in wl["matrices"] if not os.path.exists(cache_path(m))]
+    enc_s = {}
+    if todo:
+        with mp.get_context("spawn").Pool(min(len(todo), os.cpu_count() or 1)) as pool:
+            for m, dt in zip(todo, pool.starmap(_ref_encode_worker, [(m, cache_path(m)) for m in todo])):
+                enc_s[m[0]] = round(dt, 1)
+    ecs, hash_ok = {}, {}
+    for m in wl["matrices"]:
+        with open(cache_path(m), "rb") as fh:
+            blob = fh.read()
+        want = hashes.get(matrix_key(m), {}).get("sha256")
+        hash_ok[m[0]] = (sha256(blob) == want) if want else None
+        ecs[m[0]] = storage.deserialize(blob)
+    step_bytes = sum(model_bytes(ec) for ec in ecs.values())
+    xs16 = launch_inputs(HEADLINE)
+    xin = {}
+    for ln, names in wl["launches"]:
+        for n in names:
+            xin[n] = xs16[ln].astype(np.float32)
+    # 2. the stock single-process executor over the layer, W warm-up + K timed steps
+    order = [m[0] for m in wl["matrices"]]
+
+    def layer():
+        return {n: executor.spmv_ec(ecs[n], xin[n], validate=False) for n in order}
+
+    for _ in range(args.warmup):
+        y_ref = layer()
+    per = {n: 0.0 for n in order}
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for n in order:
+            a = time.perf_counter()
+            executor.spmv_ec(ecs[n], xin[n], validate=False)
+            per[n] += time.perf_counter() - a
+    step_s = (time.perf_counter() - t0) / args.steps
+    value = step_bytes / step_s / 1e9
+    # 3. secondary: all host cores, block sets split into groups (one process each); the
+    #    groups' partial y are summed and checked against the single-process y
+    cores = os.cpu_count() or 1
+    tasks = []
+    for n in order:
+        ec = ecs[n]
+        k = max(1, min(len(ec.sets), round(cores * model_bytes(ec) / step_bytes)))
+        groups, load = [[] for _ in range(k)], [0] * k
+        for i in sorted(range(len(ec.sets)), key=lambda i: -ec.sets[i].stored_cols * ec.sets[i].granularity):
+            j = load.index(min(load))
+            groups[j].append(i)
+            load[j] += ec.sets[i].stored_cols * ec.sets[i].granularity
+        tasks += [(n, sorted(g)) for g in groups if g]
+    mats = {m[0]: m for m in wl["matrices"]}
+    procs = min(len(tasks), cores)
+    reps = max(1, args.steps)
+    with mp.get_context("spawn").Pool(procs) as pool:
+        res = pool.starmap(_ref_spmv_worker, [(mats[n], g, xin[n], reps) for n, g in tasks])
+    t_sum = time.perf_counter()
+    ysum = {n: np.zeros(ecs[n].num_rows, np.float32) for n in order}
+    for (n, _), (_, y) in zip(tasks, res):
+        ysum[n] += y
+    t_sum = time.perf_counter() - t_sum
+    par_s = max(t for t, _ in res) + t_sum
+    par_err = max(float(np.max(np.abs(ysum[n] - y_ref[n])) / max(float(np.max(np.abs(y_ref[n]))), 1e-30))
+                  for n in order)
+    libs = loaded_native_libs()
+    if any("libecsr_b200" in p for p in libs):
+        raise SystemExit(f"reference arm loaded this repo's library: {libs}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(HEADLINE, step_bytes),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": 1, "kind": "reference",
+                         "sample": f"{args.steps} steps x the full layer (7 SpMVs, {step_bytes / 1e6:.1f} MB "
+                                   f"model bytes): stock ecsr.executor.spmv_ec(validate=False), "
+                                   f"backend '{backend}', single process (GIL-held kernel) on 1 of {cores} cores"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "us_per_spmv": {n: round(per[n] / args.steps * 1e6, 1) for n in order},
+        "all_cores": {"value": round(step_bytes / par_s / 1e9, 3), "unit": "GB/s",
+                      "ms_per_step": round(par_s * 1e3, 3), "processes": procs, "groups": len(tasks),
+                      "partial_y_summed": True, "rel_inf_vs_single_process": par_err,
+                      "note": "secondary: each matrix's block sets split into groups, one process "
+                              "each; step = slowest group + the partial-y sum"},
+        "inputs": {"encoder": "reference storage.convert_csr (baseline/_ref), cached in cache/",
+                   "encode_s": enc_s, "sha256_matches_pinned": hash_ok},
+        "native_so_loaded": libs,
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------
-# CPU reference path (oracle/_ref: the reference's compiled kernel), test/bench only
+# Our arm
 # ------------------------------------------------------------------------------------
 
-def _ref_set_fn():
+def load_workload(name=HEADLINE):
+    """Containers of a workload: cache/*.ecsr (reference encodings) when present, else
+    the native encoder; every blob's sha256 is checked against the pinned reference
+    hash (a mismatch stops the bench)."""
+    from paper_2507_12205_b200.container import deserialize, serialize
+    from paper_2507_12205_b200.encoder import convert_csr
+    from paper_2507_12205_b200.generators import make_matrix
+
+    hashes = ref_hashes()
+    ecs, src, ok = {}, {}, {}
+    for m in WORKLOADS[name]["matrices"]:
+        path = cache_path(m)
+        if os.path.exists(path):
+            with open(path, "rb") as fh:
+                blob = fh.read()
+            ecs[m[0]] = deserialize(blob)
+            src[m[0]] = "cache"
+        else:
+            _, kind, rows, cols, s, seed = m
+            ecs[m[0]] = convert_csr(make_matrix(kind, rows, cols, s, seed, dtype=np.float32))
+            blob = serialize(ecs[m[0]])
+            src[m[0]] = "native-encoder"
+            try:
+                os.makedirs(os.path.dirname(path), exist_ok=True)
+                with open(path + f".tmp{os.getpid()}", "wb") as fh:
+                    fh.write(blob)
+                os.replace(path + f".tmp{os.getpid()}", path)
+            except OSError:
+                pass
+        want = hashes.get(matrix_key(m), {}).get("sha256")
+        ok[m[0]] = None if want is None else sha256(blob) == want
+        if ok[m[0]] is False:
+            raise SystemExit(f"{matrix_key(m)}: encoding differs from the pinned reference encoding")
+    return ecs, {"source": src, "sha256_matches_pinned": ok}
+
+
+def check_parity(name, ecs, handles, xs, ys, stream):
+    """Every launch of the workload against the oracle (the reference kernel's
+    arithmetic, oracle/liboracle.so): ordered mode bitwise on fp16-rounded inputs, fast
+    mode rel-inf <= 1e-5 of that and rel-L2 <= 1e-3 of the FP32 result (north_star)."""
+    import torch
+
     import oracle
+    from paper_2507_12205_b200.device import spmv
 
-    ref = oracle.load_reference_speedups()
-    if ref is not None:
-        return ref.spmv_set, "reference"
-    return oracle.spmv_set, "port"
+    out = {}
+    for ln, names in WORKLOADS[name]["launches"]:
+        x16 = xs[ln].cpu().numpy()
+        x32 = x16.astype(np.float32)
+        y16 = np.concatenate([oracle.spmv_ec_oracle(ecs[n].astype(np.float16).astype(np.float32), x32,
+                                                    np.float32) for n in names])
+        y32 = np.concatenate([oracle.spmv_ec_oracle(ecs[n].astype(np.float32), x32, np.float32)
+                              for n in names])
+        spmv(handles[ln], xs[ln], y=ys[ln], ordered=True, stream=stream)
+        torch.cuda.synchronize()
+        y_ord = ys[ln].cpu().numpy()
+        spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
+        torch.cuda.synchronize()
+        y_fast = ys[ln].cpu().numpy()
+        scale = max(float(np.max(np.abs(y16))), 1e-30)
+        rel_inf = float(np.max(np.abs(y_fast.astype(np.float64) - y16))) / scale
+        rel_l2 = float(np.linalg.norm(y_fast.astype(np.float64) - y32) / max(np.linalg.norm(y32), 1e-30))
+        bitwise = bool(np.array_equal(y_ord, y16))
+        out[ln] = {"ordered_bitwise": bitwise, "fast_rel_inf": rel_inf, "fast_rel_l2_vs_fp32": rel_l2}
+        if not bitwise or rel_inf > 1e-5 or rel_l2 > 1e-3:
+            raise SystemExit(f"parity guard failed on {name}/{ln}: {out[ln]}")
+    return out
 
 
-def _cpu_spmv_once(name, reps, sets=None):
-    """Worker: reps x executor.spmv_ec(ec_f32, x_f32, validate=False) on one matrix (or
-    on a subset of its block sets: the sets' contributions to y simply add up)."""
+class Workload:
+    """Device handles, inputs and outputs of one workload (x and y of every launch are
+    16-B aligned slices of one pinned host / one device buffer)."""
+
+    def __init__(self, name, dev):
+        import torch
+
+        from paper_2507_12205_b200 import to_device
+        from paper_2507_12205_b200.device import vstack
+
+        self.name = name
+        self.launches = WORKLOADS[name]["launches"]
+        self.ecs, self.inputs = load_workload(name)
+        self.mbytes = {n: model_bytes(ec) for n, ec in self.ecs.items()}
+        self.step_bytes = sum(self.mbytes.values())
+        self.launch_bytes = {ln: sum(self.mbytes[n] for n in names) for ln, names in self.launches}
+        self.handles = {ln: to_device(vstack([self.ecs[n] for n in names]), device=dev)
+                        for ln, names in self.launches}
+        xs16 = launch_inputs(name)
+
+        def pad8(n):
+            return (n + 7) // 8 * 8
+
+        kx = [pad8(len(xs16[ln])) for ln, _ in self.launches]
+        my = [pad8(self.handles[ln].num_rows) for ln, _ in self.launches]
+        self.x_host_all = torch.zeros(sum(kx), dtype=torch.float16).pin_memory()
+        self.y_host_all = torch.zeros(sum(my), dtype=torch.float32).pin_memory()
+        self.xs_host, self.ys_host, xo, yo = {}, {}, 0, 0
+        for (ln, _), k, mm in zip(self.launches, kx, my):
+            self.x_host_all[xo:xo + len(xs16[ln])] = torch.from_numpy(xs16[ln])
+            self.xs_host[ln] = self.x_host_all[xo:xo + len(xs16[ln])]
+            self.ys_host[ln] = self.y_host_all[yo:yo + self.handles[ln].num_rows]
+            xo, yo = xo + k, yo + mm
+        self.x_all = self.x_host_all.to(dev)
+        self.y_all = torch.zeros(self.y_host_all.shape, dtype=torch.float32, device=dev)
+        self.xs, self.ys, xo, yo = {}, {}, 0, 0
+        for (ln, _), k, mm in zip(self.launches, kx, my):
+            self.xs[ln] = self.x_all[xo:xo + len(xs16[ln])]
+            self.ys[ln] = self.y_all[yo:yo + self.handles[ln].num_rows]
+            xo, yo = xo + k, yo + mm
+
+    def step(self, stream):
+        from paper_2507_12205_b200.device import spmv
+
+        for ln, _ in self.launches:
+            spmv(self.handles[ln], self.xs[ln], y=self.ys[ln], stream=stream)
+
+    def graph(self, stream, steps):
+        import torch
+
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                self.step(stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(steps):
+                self.step(stream)
+        return g
+
+
+def time_graph(g, replays, warmup, stream, flush=None):
+    """Device time per replay (CUDA events on the launching stream). With `flush`, a
+    512 MB buffer is rewritten between replays (L2 is 126 MB) and each replay is timed
+    on its own; returns (mean, per-replay list)."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            if flush is not None:
+                flush.add_(1)
+            g.replay()
+    torch.cuda.synchronize()
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(replays):
+                g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / replays, []
+    ts = []
+    with torch.cuda.stream(stream):
+        for _ in range(replays):
+            flush.add_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+    return sum(ts) / len(ts), ts
+
+
+def bench_extra(name, dev, stream, args, peak):
+    """Another BASELINE config, timed like the headline (parity-checked first)."""
+    import torch
+
+    t0 = time.perf_counter()
+    wl = Workload(name, dev)
+    setup_s = time.perf_counter() - t0
+    par = check_parity(name, wl.ecs, wl.handles, wl.xs, wl.ys, stream)
+    out = {"workload": name, "desc": WORKLOADS[name]["desc"],
+           "config": workload_config(name, wl.step_bytes), "parity": par,
+           "inputs": wl.inputs, "setup_s": round(setup_s, 1)}
+    if wl.step_bytes > 126e6:
+        spg = 5
+        g = wl.graph(stream, spg)
+        ms, _ = time_graph(g, max(2, args.steps // spg), 2, stream)
+        ms /= spg
+        gbs = wl.step_bytes / (ms * 1e-3) / 1e9
+        out.update({"value": round(gbs, 1), "unit": "GB/s", "ms_per_step": round(ms, 5),
+                    "frac": round(gbs / peak, 4), "steps_per_graph": spg})
+    else:
+        g = wl.graph(stream, 1)
+        flush = torch.empty(128 << 20, dtype=torch.float32, device=dev)
+        ms, ts = time_graph(g, max(20, args.steps), 3, stream, flush=flush)
+        ts.sort()
+        gbs = wl.step_bytes / (ms * 1e-3) / 1e9
+        out.update({"value": round(gbs, 1), "unit": "GB/s", "latency_us": round(ms * 1e3, 2),
+                    "latency_us_p10_p50_p90": [round(ts[int(q * (len(ts) - 1))] * 1e3, 2) for q in (0.1, 0.5, 0.9)],
+                    "frac": round(gbs / peak, 4), "cold_l2": True})
+    del wl
+    torch.cuda.synchronize()
+    return out
+
+
+def _cpu_spmv_once(m, reps):
+    """Worker: reps x executor.spmv_ec(ec_f32, x_f32, validate=False) over the C kernel
+    compiled from the reference's _speedups.pyx (oracle/_ref), else the oracle port."""
     import oracle
+    from paper_2507_12205_b200.container import load_container
 
-    from paper_2507_12205_b200.container import EcCsrMatrix, load_container
-
-    ec = load_container(cache_path(name)).astype(np.float32)
-    if sets is not None:
-        ec = EcCsrMatrix(ec.num_rows, ec.num_cols, ec.value_bits, ec.delta_bits, ec.warp_size,
-                         [ec.sets[i] for i in sets])
+    ec = load_container(cache_path(m)).astype(np.float32)
     x = np.random.default_rng(5000).uniform(-1, 1, ec.num_cols).astype(np.float32)
-    fn, kind = _ref_set_fn()
+    ref = oracle.load_reference_speedups()
+    fn, kind = (ref.spmv_set, "reference") if ref is not None else (oracle.spmv_set, "port")
     oracle.spmv_ec_oracle(ec, x, np.float32, set_fn=fn)  # warm-up (cli.py:235-240 method)
     t0 = time.perf_counter()
     for _ in range(reps):
@@ -205,17 +617,14 @@ def _cpu_spmv_once(name, reps, sets=None):
 
 def cpu_baseline(mbytes, budget_s=10.0):
     """One core, the reference kernel, the whole layer repeated for ~budget_s."""
-    per = {}
-    kind = "reference"
-    for name, *_ in MATRICES:
-        t, kind = _cpu_spmv_once(name, 1)
-        per[name] = t
+    mats = WORKLOADS[HEADLINE]["matrices"]
+    per, kind = {}, "reference"
+    for m in mats:
+        per[m[0]], kind = _cpu_spmv_once(m, 1)
     layer = sum(per.values())
     reps = max(1, int(budget_s / max(layer, 1e-6)))
-    per = {}
-    for name, *_ in MATRICES:
-        t, kind = _cpu_spmv_once(name, reps)
-        per[name] = t
+    for m in mats:
+        per[m[0]], kind = _cpu_spmv_once(m, reps)
     layer = sum(per.values())
     total = sum(mbytes.values())
     return {"value": round(total / layer / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": kind,
@@ -225,59 +634,156 @@ def cpu_baseline(mbytes, budget_s=10.0):
             "us_per_spmv": {k: round(v * 1e6, 1) for k, v in per.items()}}
 
 
-def run_reference(args):
-    rank, _, world = dist_env()
-    if rank != 0:
-        return
-    import multiprocessing as mp
+def run_ours(args):
+    import torch
 
-    ecs, _ = load_workload()
-    mbytes = model_bytes(ecs)
-    # The reference kernel is single-threaded (GIL held, _speedups.pyx:81-129); to use the
-    # host's cores, each matrix's block sets are split into groups (their y contributions
-    # add up), one process per group, ~one group per core, sets balanced by stored bytes.
-    cores = os.cpu_count() or 1
-    total = sum(mbytes.values())
-    tasks = []
-    for name, *_ in MATRICES:
-        ec = ecs[name]
-        k = max(1, min(len(ec.sets), round(cores * mbytes[name] / total)))
-        groups = [[] for _ in range(k)]
-        load = [0] * k
-        for i in sorted(range(len(ec.sets)), key=lambda i: -ec.sets[i].stored_cols * ec.sets[i].granularity):
-            j = load.index(min(load))
-            groups[j].append(i)
-            load[j] += ec.sets[i].stored_cols * ec.sets[i].granularity
-        tasks += [(name, sorted(gr)) for gr in groups if gr]
-    del ecs
-    procs = min(len(tasks), cores)
-    # one warm-up step, then K timed steps of the whole layer (all groups concurrently)
-    with mp.get_context("spawn").Pool(procs) as pool:
-        pool.starmap(_cpu_spmv_once, [(n, 1, gr) for n, gr in tasks])
-        t0 = time.perf_counter()
-        res = pool.starmap(_cpu_spmv_once, [(n, args.steps, gr) for n, gr in tasks])
-        wall = time.perf_counter() - t0
-    kind = res[0][1]
-    step_s = max(t for t, _ in res)  # the groups run concurrently
-    value = total / step_s / 1e9
+    rank, local_rank, world = dist_env()
+    if world > 1 or args.shard:
+        return run_sharded(args)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    peak, peak_kind = peaks()
+
+    wl = Workload(HEADLINE, dev)
+    stream = torch.cuda.Stream(dev)
+    parity = check_parity(HEADLINE, wl.ecs, wl.handles, wl.xs, wl.ys, stream)
+
+    # device-resident timing: a CUDA graph of `spg` consecutive steps (layers), replayed
+    # steps/spg times -- a decode graph holds a model's consecutive layers, so launches
+    # chain through PDL across layers as they do in deployment; exactly K steps are timed
+    spg = max(d for d in range(1, 9) if args.steps % d == 0)
+    graph = wl.graph(stream, spg)
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup // spg)):
+            graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks, torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps // spg):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+
+    # per-launch device time of each launch kind: a graph of that launch alone, replayed
+    # after the whole layer (284 MB > L2) streamed through, CUDA events around it
+    from paper_2507_12205_b200.device import spmv
+
+    launch_ms = {}
+    for ln, _ in wl.launches:
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=stream):
+            spmv(wl.handles[ln], wl.xs[ln], y=wl.ys[ln], stream=stream)
+        n = max(5, args.steps // 2)
+        tot = 0.0
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                g1.replay()
+                graph.replay()
+            for _ in range(n):
+                graph.replay()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g1.replay()
+                b.record(stream)
+                b.synchronize()
+                tot += a.elapsed_time(b)
+        launch_ms[ln] = tot / n
+
+    # end-to-end through the public API: pinned host x in, y out, every step. The first
+    # launch's x and the last launch's y are on the critical path; the other inputs go
+    # up, and the other outputs come back, on a side stream while launches run.
+    h2d = sum(x.numel() * 2 for x in wl.xs_host.values())
+    d2h = sum(y.numel() * 4 for y in wl.ys_host.values())
+    side = torch.cuda.Stream(dev)
+    first, last = wl.launches[0][0], wl.launches[-1][0]
+    k0 = wl.xs[first].numel()
+    y_last0 = wl.ys[last].data_ptr() - wl.y_all.data_ptr()
+    y_last0 //= 4
+
+    def e2e_body():
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        side.wait_event(fork)
+        wl.x_all[:k0].copy_(wl.x_host_all[:k0], non_blocking=True)
+        with torch.cuda.stream(side):
+            wl.x_all[k0:].copy_(wl.x_host_all[k0:], non_blocking=True)
+            x_rest = torch.cuda.Event()
+            x_rest.record(side)
+        head_done = torch.cuda.Event()
+        for i, (ln, _) in enumerate(wl.launches):
+            if i == 1:
+                stream.wait_event(x_rest)
+            spmv(wl.handles[ln], wl.xs[ln], y=wl.ys[ln], stream=stream)
+            if i == len(wl.launches) - 2:
+                head_done.record(stream)
+        with torch.cuda.stream(side):
+            side.wait_event(head_done)
+            wl.y_host_all[:y_last0].copy_(wl.y_all[:y_last0], non_blocking=True)
+            y_head = torch.cuda.Event()
+            y_head.record(side)
+        wl.y_host_all[y_last0:].copy_(wl.y_all[y_last0:], non_blocking=True)
+        stream.wait_event(y_head)  # join
+
+    # the same step with its host<->device copies, captured once (pinned-host memcpy
+    # nodes + the 4 launches) so host API overhead does not dominate ~70 us steps
+    g_e2e = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_e2e, stream=stream):
+        e2e_body()
+    e2e_ms, _ = time_graph(g_e2e, args.steps, args.warmup, stream)
+    for ln, _ in wl.launches:  # the copies really happened
+        if not torch.equal(wl.ys_host[ln], wl.ys[ln].cpu()):
+            raise SystemExit("e2e graph did not copy y back to the host")
+
+    achieved = wl.step_bytes / (ms * 1e-3) / 1e9
+    # traffic: ncu dram__bytes_read + write of the kernel, per launch like `achieved`
+    # (the committed capture's per-step total over the step's launches)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            per_step = json.load(fh).get("dram_bytes_per_step")
+        if per_step:
+            traffic = round(per_step / len(wl.launches))
+    layout = {ln: W.bytes() for ln, W in wl.handles.items()}
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "metric": METRIC,
+        "value": round(wl.step_bytes / (ms * 1e-3) / 1e9, 1), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "matrices": [m[:6] for m in MATRICES],
-                   "encoder": "reference convert_csr W=32 V=4 B=8", "parallelism": "cpu"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": procs, "kind": kind,
-                         "sample": f"{args.steps} steps x 7 SpMVs as {len(tasks)} set groups, one "
-                                   f"process each on {procs} of {cores} cores, wall {wall:.1f}s"},
-        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 values/x, f32 accumulate", "data": "synthetic",
+        "config": workload_config(HEADLINE, wl.step_bytes),
+        "steps_per_graph": spg, "parallelism": "single",
+        "latency_us": {ln: round(v * 1e3, 2) for ln, v in launch_ms.items()},
+        "e2e": {"value": round(wl.step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+                "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": round(wl.step_bytes / len(wl.launches)),
+                     "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel",
+                     "device_arena_bytes": {ln: layout[ln]["device_arena_bytes"] for ln in layout}},
+        "parity": parity,
+        "inputs": wl.inputs,
+        "gpu_launches": len(wl.launches) * args.steps,
+        "clocks": clocks.summary(),
     }
+    mbytes = dict(wl.mbytes)
+    del wl, graph, g_e2e
+    torch.cuda.synchronize()
+    if not args.no_extra:
+        line["configs"] = [bench_extra(n, dev, stream, args, peak)
+                           for n in WORKLOADS if n != HEADLINE]
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(mbytes, budget_s=args.cpu_budget)
+    line["native_so_loaded"] = loaded_native_libs()
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------
-# GPU path
+# Multi-GPU: row shards + NCCL
 # ------------------------------------------------------------------------------------
 
 def load_shards(rank, world):
@@ -289,15 +795,16 @@ def load_shards(rank, world):
     from paper_2507_12205_b200.sharded import row_slice, shard_bounds
 
     ecs, bounds = {}, {}
-    for name, kind, rows, cols, s, seed, _ in MATRICES:
-        m = make_matrix(kind, rows, cols, s, seed, dtype=np.float32)
-        b = shard_bounds(m.row_ptr, world)
+    for m in WORKLOADS[HEADLINE]["matrices"]:
+        name, kind, rows, cols, s, seed = m
+        a = make_matrix(kind, rows, cols, s, seed, dtype=np.float32)
+        b = shard_bounds(a.row_ptr, world)
         bounds[name] = b
-        path = cache_path(name)[:-5] + f"_shard{rank}of{world}.ecsr"
+        path = cache_path(m)[:-5] + f"_shard{rank}of{world}.ecsr"
         if os.path.exists(path):
             ecs[name] = load_container(path)
             continue
-        ecs[name] = convert_csr(row_slice(m, b[rank], b[rank + 1]))
+        ecs[name] = convert_csr(row_slice(a, b[rank], b[rank + 1]))
         try:
             os.makedirs(os.path.dirname(path), exist_ok=True)
             save_container(ecs[name], path + f".tmp{os.getpid()}")
@@ -309,12 +816,12 @@ def load_shards(rank, world):
 
 def run_sharded(args):
     """N > 1: every matrix row-sharded over the ranks (byte-balanced, shard-first),
-    x replicated, y all-gathered over NCCL after each launch (strong scaling)."""
+    x replicated; one coalesced NCCL all-gather per step assembles every launch's y
+    straight into its final layout (strong scaling)."""
     import torch
     import torch.distributed as dist
 
     from paper_2507_12205_b200 import to_device
-    from paper_2507_12205_b200.container import kernel_model_bytes
     from paper_2507_12205_b200.device import spmv, vstack
     from paper_2507_12205_b200.sharded import ShardPlan
 
@@ -331,151 +838,130 @@ def run_sharded(args):
     json_fd = os.dup(1)
     os.dup2(2, 1)
     dist.init_process_group("nccl", device_id=dev)
+    launches = WORKLOADS[HEADLINE]["launches"]
     ecs, bounds = load_shards(rank, world)
-    local_bytes = sum(kernel_model_bytes(ec) for ec in ecs.values())
+    local_bytes = sum(model_bytes(ec) for ec in ecs.values())
     t = torch.tensor([float(local_bytes)], device=dev, dtype=torch.float64)
     dist.all_reduce(t)
     step_bytes = int(t.item())
-    plans = {ln: ShardPlan([bounds[n] for n in names], names) for ln, names in LAUNCHES}
-    handles = {ln: to_device(vstack([ecs[n] for n in names])) for ln, names in LAUNCHES}
-    kdim = {"qkv": 4096, "o": 4096, "gate_up": 4096, "down": 11008}
-    rng = np.random.default_rng(5000)
-    xs_host = {ln: torch.from_numpy(rng.uniform(-1, 1, kdim[ln]).astype(np.float16)).pin_memory()
-               for ln, _ in LAUNCHES}
+    plans = {ln: ShardPlan([bounds[n] for n in names], names) for ln, names in launches}
+    handles = {ln: to_device(vstack([ecs[n] for n in names])) for ln, names in launches}
+    xs16 = launch_inputs(HEADLINE)
+    xs_host = {ln: torch.from_numpy(xs16[ln]).pin_memory() for ln, _ in launches}
     xs = {ln: xs_host[ln].to(dev) for ln in xs_host}
-    ypad = {ln: torch.zeros(plans[ln].max_rows(), dtype=torch.float32, device=dev) for ln in plans}
-    yall = {ln: torch.empty(world * plans[ln].max_rows(), dtype=torch.float32, device=dev) for ln in plans}
-    yall_host = {ln: torch.empty(yall[ln].shape, dtype=torch.float32).pin_memory() for ln in yall}
+    # y of every launch: one padded slot of max_rows per rank in a flat send buffer; one
+    # all-gather per step; the final per-launch y is an index gather (identity when the
+    # shards have equal rows, the usual case for uniformly pruned matrices)
+    slot = {ln: plans[ln].max_rows() for ln, _ in launches}
+    offs, o = {}, 0
+    for ln, _ in launches:
+        offs[ln] = o
+        o += slot[ln]
+    send = torch.zeros(o, dtype=torch.float32, device=dev)
+    recv = torch.empty(world * o, dtype=torch.float32, device=dev)
+    gidx = {}
+    for ln, _ in launches:
+        idx = []
+        pl = plans[ln]
+        for i, b in enumerate(pl.bounds):
+            for r in range(world):
+                within = sum(bb[r + 1] - bb[r] for bb in pl.bounds[:i])
+                idx.append(r * o + offs[ln] + within + np.arange(b[r + 1] - b[r]))
+        gidx[ln] = torch.from_numpy(np.concatenate(idx)).to(dev)
+    yfull = {ln: torch.empty(int(gidx[ln].numel()), dtype=torch.float32, device=dev) for ln, _ in launches}
+    yfull_host = {ln: torch.empty(yfull[ln].shape, dtype=torch.float32).pin_memory() for ln in yfull}
     stream = torch.cuda.Stream(dev)
 
+    def spmvs():
+        for ln, _ in launches:
+            spmv(handles[ln], xs[ln], y=send[offs[ln]:offs[ln] + handles[ln].num_rows], stream=stream)
+
+    def exchange():
+        dist.all_gather_into_tensor(recv, send)
+        for ln, _ in launches:
+            torch.index_select(recv, 0, gidx[ln], out=yfull[ln])
+
     def step():
-        for ln, _ in LAUNCHES:
-            spmv(handles[ln], xs[ln], y=ypad[ln][:handles[ln].num_rows], stream=stream)
-            dist.all_gather_into_tensor(yall[ln], ypad[ln])
+        spmvs()
+        exchange()
 
     with torch.cuda.stream(stream):
         for _ in range(3):
             step()
     torch.cuda.synchronize()
-    # parity guard: the gathered o output equals the oracle on this rank's shard rows
+    # parity guard: every launch's assembled y on this rank vs the oracle over this
+    # rank's shard rows (bitwise in ordered mode is checked by the -m gpu tests)
     import oracle
 
-    ec16 = ecs["o"].astype(np.float16).astype(np.float32)
-    ref = oracle.spmv_ec_oracle(ec16, xs_host["o"].numpy().astype(np.float32), np.float32)
-    mr = plans["o"].max_rows()
-    got = yall["o"][rank * mr: rank * mr + ec16.num_rows].cpu().numpy()
-    rel = float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30))
-    if rel > 1e-5:
-        raise SystemExit(f"parity guard failed on rank {rank}: rel-inf {rel:.3e}")
+    for ln, names in launches:
+        pl = plans[ln]
+        got = yfull[ln].cpu().numpy()
+        base = 0
+        for i, n in enumerate(names):
+            b = pl.bounds[i]
+            ref = oracle.spmv_ec_oracle(ecs[n].astype(np.float16).astype(np.float32),
+                                        xs16[ln].astype(np.float32), np.float32)
+            seg = got[base + b[rank]: base + b[rank + 1]]
+            rel = float(np.max(np.abs(seg - ref)) / max(float(np.max(np.abs(ref))), 1e-30))
+            if rel > 1e-5:
+                raise SystemExit(f"parity guard failed on rank {rank} {ln}/{n}: rel-inf {rel:.3e}")
+            base += b[-1]
 
-    graph = None
-    try:  # NCCL collectives are capturable; fall back to eager launches if not
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            step()
-        graph = g
-    except Exception:  # noqa: BLE001
-        graph = None
-        torch.cuda.synchronize()
-
-    def run_steps(n):
-        with torch.cuda.stream(stream):
-            for _ in range(n):
-                if graph is not None:
-                    graph.replay()
-                else:
-                    step()
-
-    run_steps(args.warmup)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clocks:
-        e0.record(stream)
-        run_steps(args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-
-    def e2e_body():
-        for ln, _ in LAUNCHES:
-            xs[ln].copy_(xs_host[ln], non_blocking=True)
-        step()
-        for ln, _ in LAUNCHES:
-            yall_host[ln].copy_(yall[ln], non_blocking=True)
-
-    g_e2e = None
-    if graph is not None:
+    def capture(body):
         try:
-            g_e2e = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_e2e, stream=stream):
-                e2e_body()
-        except Exception:  # noqa: BLE001
-            g_e2e = None
-            torch.cuda.synchronize()
-
-    def e2e_steps(n):
-        with torch.cuda.stream(stream):
-            for _ in range(n):
-                if g_e2e is not None:
-                    g_e2e.replay()
-                else:
-                    e2e_body()
-
-    e2e_steps(args.warmup)
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    e2e_steps(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    # the step's two halves timed apart (SURVEY.md §8(e) reporting): the per-GPU shard
-    # SpMVs alone and the y all-gathers alone, each as its own graph when capturable
-    def split_ms(body):
-        try:
-            g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2, stream=stream):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
                 body()
-            run = g2.replay
-        except Exception:  # noqa: BLE001
+            return g.replay
+        except Exception:  # noqa: BLE001 -- NCCL capture unsupported: eager launches
             torch.cuda.synchronize()
-            run = body
+            return body
+
+    def timed(run):
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
                 run()
         dist.barrier()
         torch.cuda.synchronize()
-        e0.record(stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
+            e0.record(stream)
             for _ in range(args.steps):
                 run()
-        e1.record(stream)
+            e1.record(stream)
         torch.cuda.synchronize()
+        dist.barrier()
         return e0.elapsed_time(e1) / args.steps
 
-    spmv_ms = split_ms(lambda: [spmv(handles[ln], xs[ln], y=ypad[ln][:handles[ln].num_rows], stream=stream)
-                                for ln, _ in LAUNCHES])
-    gather_ms = split_ms(lambda: [dist.all_gather_into_tensor(yall[ln], ypad[ln]) for ln, _ in LAUNCHES])
+    run_step = capture(step)
+    with ClockSampler(local_rank) as clocks:
+        ms = timed(run_step)
+
+    def e2e_body():
+        for ln, _ in launches:
+            xs[ln].copy_(xs_host[ln], non_blocking=True)
+        step()
+        for ln, _ in launches:
+            yfull_host[ln].copy_(yfull[ln], non_blocking=True)
+
+    e2e_ms = timed(capture(e2e_body))
+    spmv_ms = timed(capture(spmvs))
+    gather_ms = timed(capture(exchange))
     t = torch.tensor([ms, e2e_ms, spmv_ms, gather_ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, e2e_ms, spmv_ms, gather_ms = t.tolist()
     if rank == 0:
         peak, peak_kind = peaks()
         h2d = sum(x.numel() * 2 for x in xs_host.values())
-        d2h = sum(y.numel() * 4 for y in yall_host.values())
+        d2h = sum(y.numel() * 4 for y in yfull_host.values())
+        cfg = workload_config(HEADLINE, step_bytes)
+        cfg["encoder"] = "shard-first native convert_csr W=32 V=4 B=8 (row slice encoded alone)"
         line = {
             "metric": METRIC, "value": round(step_bytes / (ms * 1e-3) / 1e9, 1), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16 values/x, f32 accumulate", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "matrices": [m[:6] for m in MATRICES],
-                       "launches_per_step": [ln for ln, _ in LAUNCHES],
-                       "model_bytes_per_step": step_bytes,
-                       "encoder": "shard-first native convert_csr W=32 V=4 B=8",
-                       "parallelism": f"row-shard{world}+nccl-allgather",
-                       "graph": graph is not None},
+            "config": cfg, "parallelism": f"row-shard{world}+nccl-allgather",
             "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -483,234 +969,15 @@ def run_sharded(args):
                          "peak": peak, "unit": "GB/s per GPU",
                          "frac": round(step_bytes / world / (ms * 1e-3) / 1e9 / peak, 4),
                          "traffic": None, "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel"},
-            "gpu_launches": len(LAUNCHES) * args.steps,
+            "gpu_launches": len(launches) * args.steps,
             "clocks": clocks.summary(),
-            "sharded": {"spmv_ms_per_step": round(spmv_ms, 5), "allgather_ms_per_step": round(gather_ms, 5),
-                        "step_ms": round(ms, 5), "allgather_bytes_per_rank_per_step":
-                        sum(int(ypad[ln].numel()) * 4 for ln in ypad)},
+            "sharded": {"spmv_ms_per_step": round(spmv_ms, 5), "exchange_ms_per_step": round(gather_ms, 5),
+                        "step_ms": round(ms, 5), "allgather_bytes_per_rank_per_step": int(send.numel()) * 4,
+                        "collectives_per_step": 1, "y_assembled_in_step": True},
         }
         sys.stdout.flush()
         os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.destroy_process_group()
-
-
-def run_ours(args):
-    import torch
-
-    rank, local_rank, world = dist_env()
-    if world > 1 or args.shard:
-        return run_sharded(args)
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    from paper_2507_12205_b200 import to_device
-    from paper_2507_12205_b200.device import spmv, vstack
-
-    ecs, sources = load_workload()
-    mbytes = model_bytes(ecs)
-    step_bytes = sum(mbytes.values())
-    launch_bytes = {ln: sum(mbytes[n] for n in names) for ln, names in LAUNCHES}
-    handles = {ln: to_device(vstack([ecs[n] for n in names])) for ln, names in LAUNCHES}
-    layout = {ln: W.bytes() for ln, W in handles.items()}
-    inputs = {"qkv": "x_attn", "o": "x_o", "gate_up": "x_mlp", "down": "x_down"}
-    kdim = {"qkv": 4096, "o": 4096, "gate_up": 4096, "down": 11008}
-    rng = np.random.default_rng(5000 + rank)
-    # every launch's x (and y) is a 16-B aligned slice of one pinned host buffer and one
-    # device buffer, so the end-to-end step moves its inputs and outputs with one H2D and
-    # one D2H copy instead of one per launch
-    x_host_all = torch.from_numpy(np.concatenate(
-        [rng.uniform(-1, 1, kdim[ln]).astype(np.float16) for ln, _ in LAUNCHES])).pin_memory()
-    x_all = x_host_all.to(dev)
-    y_all = torch.empty(sum(handles[ln].num_rows for ln, _ in LAUNCHES), dtype=torch.float32, device=dev)
-    y_host_all = torch.empty(y_all.shape, dtype=torch.float32).pin_memory()
-    xs_host, xs, ys, ys_host = {}, {}, {}, {}
-    xo = yo = 0
-    for ln, _ in LAUNCHES:
-        k, m = kdim[ln], handles[ln].num_rows
-        xs_host[ln], xs[ln] = x_host_all[xo:xo + k], x_all[xo:xo + k]
-        ys_host[ln], ys[ln] = y_host_all[yo:yo + m], y_all[yo:yo + m]
-        xo, yo = xo + k, yo + m
-    stream = torch.cuda.Stream(dev)
-
-    def step():
-        for ln, _ in LAUNCHES:
-            spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
-
-    # correctness guard (cheap): o = W_o x_o against the CPU oracle on this rank's data
-    with torch.cuda.stream(stream):
-        step()
-    torch.cuda.synchronize()
-    import oracle
-
-    ec16 = ecs["o"].astype(np.float16).astype(np.float32)
-    ref = oracle.spmv_ec_oracle(ec16, xs_host["o"].numpy().astype(np.float32), np.float32)
-    got = ys["o"].cpu().numpy()
-    rel = float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30))
-    if rel > 1e-5 and not os.environ.get("ECSR_B200_LIB"):  # tuning builds may be wrong on purpose
-        raise SystemExit(f"parity guard failed: rel-inf {rel:.3e}")
-
-    # device-resident timing: a CUDA graph of `spg` consecutive steps (layers), replayed
-    # steps/spg times -- a decode graph holds a model's consecutive layers, so launches
-    # chain through PDL across layers as they do in deployment; exactly K steps are timed
-    spg_max = int(os.environ.get("ECSR_BENCH_SPG", "8"))
-    spg = max(d for d in range(1, max(1, spg_max) + 1) if args.steps % d == 0)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            step()
-    torch.cuda.synchronize()
-    with torch.cuda.graph(graph, stream=stream):
-        for _ in range(spg):
-            step()
-    with torch.cuda.stream(stream):  # replay() launches on the current stream
-        for _ in range(max(1, args.warmup // spg)):
-            graph.replay()
-    torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    with ClockSampler(local_rank) as clocks, torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(args.steps // spg):
-            graph.replay()
-        e1.record(stream)
-        barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-
-    # per-launch device time of each launch kind: a graph of that launch alone, replayed
-    # (CUDA events on the launching stream; its weights, > L2 together with the other
-    # launches' between replays, are re-streamed from HBM: evict-first L2 policy)
-    launch_ms = {}
-    for ln, _ in LAUNCHES:
-        g1 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g1, stream=stream):
-            spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
-        with torch.cuda.stream(stream):
-            for _ in range(3):
-                g1.replay()
-                graph.replay()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            tot = 0.0
-            for _ in range(max(5, args.steps // 2)):
-                graph.replay()  # flush: the whole layer (284 MB) streams through L2
-                a.record(stream)
-                g1.replay()
-                b.record(stream)
-                b.synchronize()
-                tot += a.elapsed_time(b)
-        launch_ms[ln] = tot / max(5, args.steps // 2)
-
-    # end-to-end through the public API: pinned host x in, y out, every step
-    h2d = sum(x.numel() * 2 for x in xs_host.values())
-    d2h = sum(y.numel() * 4 for y in ys_host.values())
-
-    # The first launch's x and the last launch's y are on the critical path; the other
-    # inputs go up, and the other outputs come back, on a side stream while launches run.
-    side = torch.cuda.Stream(dev)
-    k0 = kdim[LAUNCHES[0][0]]
-    m_last = handles[LAUNCHES[-1][0]].num_rows
-
-    def e2e_body():
-        fork = torch.cuda.Event()
-        fork.record(stream)
-        side.wait_event(fork)
-        x_all[:k0].copy_(x_host_all[:k0], non_blocking=True)
-        with torch.cuda.stream(side):
-            x_all[k0:].copy_(x_host_all[k0:], non_blocking=True)
-            x_rest = torch.cuda.Event()
-            x_rest.record(side)
-        ev = {}
-        for i, (ln, _) in enumerate(LAUNCHES):
-            if i == 1:
-                stream.wait_event(x_rest)
-            spmv(handles[ln], xs[ln], y=ys[ln], stream=stream)
-            if i == len(LAUNCHES) - 2:
-                ev["head_done"] = torch.cuda.Event()
-                ev["head_done"].record(stream)
-        with torch.cuda.stream(side):
-            side.wait_event(ev["head_done"])
-            y_host_all[:-m_last].copy_(y_all[:-m_last], non_blocking=True)
-            y_head = torch.cuda.Event()
-            y_head.record(side)
-        y_host_all[-m_last:].copy_(y_all[-m_last:], non_blocking=True)
-        stream.wait_event(y_head)  # join
-
-    # the same step with its host<->device copies, captured once (pinned-host memcpy
-    # nodes + the 4 launches) so the host API overhead does not dominate 100 us steps
-    g_e2e = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_e2e, stream=stream):
-        e2e_body()
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            g_e2e.replay()
-    barrier()
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(args.steps):
-            g_e2e.replay()
-        e1.record(stream)
-    barrier()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    # the copies really happened: the host y of the o launch matches the device one
-    if not torch.equal(ys_host["o"], ys["o"].cpu()):
-        raise SystemExit("e2e graph did not copy y back to the host")
-
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms, e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, e2e_ms = t.tolist()
-    if rank != 0:
-        return
-    peak, peak_kind = peaks()
-    # dominant (only) kernel: every launch of the step is ecsr_tiled_kernel, so its average
-    # launch duration over the timed region is ms / launches and the algorithmic bytes of
-    # a launch average step_bytes / launches
-    achieved = step_bytes / (ms * 1e-3) / 1e9
-    # traffic: ncu dram__bytes_read + write of the kernel, per launch like `achieved`
-    # (the committed capture's per-step total over the step's launches)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        with open(prof) as fh:
-            per_step = json.load(fh).get("dram_bytes_per_step")
-        if per_step:
-            traffic = round(per_step / len(LAUNCHES))
-    line = {
-        "metric": METRIC,
-        "value": round(world * step_bytes / (ms * 1e-3) / 1e9, 1), "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f16 values/x, f32 accumulate", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "matrices": [m[:6] for m in MATRICES],
-                   "launches_per_step": [ln for ln, _ in LAUNCHES],
-                   "model_bytes_per_step": step_bytes,
-                   "l2": "inputs 284 MB/step > 126 MB L2 (no flush)",
-                   "steps_per_graph": spg,
-                   "encoder": "convert_csr W=32 V=4 B=8 (" + "+".join(sources) + ")",
-                   "parallelism": f"replicas{world}" if world > 1 else "single"},
-        "latency_us": {ln: round(v * 1e3, 2) for ln, v in launch_ms.items()},
-        "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
-                "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_launch": round(step_bytes / len(LAUNCHES)),
-                     "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel",
-                     "device_arena_bytes": {ln: layout[ln]["device_arena_bytes"] for ln in layout}},
-        "gpu_launches": len(LAUNCHES) * args.steps,
-        "clocks": clocks.summary(),
-    }
-    if not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(mbytes, budget_s=args.cpu_budget)
-    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -721,6 +988,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--shard", action="store_true", help="use the row-sharded path even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:

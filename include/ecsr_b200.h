@@ -50,6 +50,11 @@ extern "C" {
 /* ecsr_b200_pack flags */
 #define ECSR_PACK_DEFAULT 0
 #define ECSR_PACK_FORCE_GENERIC 1 /* skip the tiled fast layout (parity/debug) */
+/* tiled layout: tile (stage) size override in KB, 1..64 (tests: many tiles per CTA) */
+#define ECSR_PACK_TILE_KB(kb) (((kb) & 0xff) << 8)
+/* tiled layout: cost share (percent, 0..100) of each CTA's tiles handed out through the
+ * launch's tail queue instead of its static range (default 5) */
+#define ECSR_PACK_QUEUE_PCT(pct) (((((pct) & 0x7f) | 0x80)) << 16)
 
 /* ecsr_b200_spmv modes */
 #define ECSR_SPMV_OVERWRITE 0   /* y  = A x */
@@ -102,9 +107,16 @@ typedef struct ecsr_bytes {
     int32_t stages;             /* smem ring depth */
     int32_t stage_bytes;
     int64_t tiles;
+    int64_t queue_tiles;        /* tiles drawn from the launch's tail queue */
 } ecsr_bytes;
 
-typedef struct ecsr_dev ecsr_dev; /* opaque; immutable after pack */
+/* Opaque handle. The packed layout is read-only after pack; each launch also writes a
+ * small workspace (zero-y grid-gate counter, ordered-mode block partials), one per
+ * CUDA stream: a handle binds up to 4 streams on first use, so launches issued on (or
+ * captured from) different streams may run concurrently, and launches on one stream
+ * are stream-ordered. A 5th stream gets ECSR_ERR_VALUE. Launches run on the device the
+ * handle was packed on, whatever the caller's current device. */
+typedef struct ecsr_dev ecsr_dev;
 
 /* Validate + pack + upload. device_dtype: ECSR_F16 (the product: fp16 values and x,
  * fp32 accumulate and y), ECSR_F32 or ECSR_F64 (generic kernel, container precision). */

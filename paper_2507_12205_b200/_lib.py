@@ -59,7 +59,7 @@ class Bytes(ctypes.Structure):
                 ("desc", c_i64), ("model_kernel_bytes", c_i64),
                 ("device_arena_bytes", c_i64), ("device_total_bytes", c_i64),
                 ("layout", c_i32), ("grid", c_i32), ("stages", c_i32),
-                ("stage_bytes", c_i32), ("tiles", c_i64)]
+                ("stage_bytes", c_i32), ("tiles", c_i64), ("queue_tiles", c_i64)]
 
     def to_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

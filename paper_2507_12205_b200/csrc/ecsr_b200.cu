@@ -38,33 +38,34 @@ int fail(int code, const std::string& msg) {
             return fail(ECSR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-// bytes of whole records per tile: 16 KB with two CTAs per SM, 32 KB with one
-// (ECSR_B200_TILE overrides, for tuning)
+// bytes of whole records per tile: 16 KB with two CTAs per SM, 32 KB with one. The
+// product library has no runtime knobs; a tuning build (-DECSR_B200_TUNING, scripts/
+// build_exp.sh, never the shipped .so) reads ECSR_B200_TILE / _PRE / _RECCAP / _RECMAX
+// and can record a per-CTA timeline (ECSR_B200_TRACE).
 int g_tile_default = 16384;
+thread_local int t_tile_override = 0;  // ECSR_PACK_TILE_KB(n) of the pack in progress
+#ifdef ECSR_B200_TUNING
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
 int tile_target() {
-    static int env = [] {
-        const char* e = std::getenv("ECSR_B200_TILE");
-        return e ? std::max(1024, std::atoi(e)) : 0;
-    }();
-    return env ? env : g_tile_default;
+    const int v = env_int("ECSR_B200_TILE", 0);
+    return t_tile_override ? t_tile_override : v ? std::max(1024, v) : g_tile_default;
 }
-int pre_tiles() {  // tiles streamed before griddepcontrol.wait and the x copy
-    static int v = [] {
-        const char* e = std::getenv("ECSR_B200_PRE");
-        return e ? std::max(1, std::atoi(e)) : 2;
-    }();
-    return v;
-}
-int debug_flags() {  // tuning experiments only: 1 = consumers skip compute, 2 = no y memset
-    static int v = [] {
-        const char* e = std::getenv("ECSR_B200_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
+int pre_tiles() { return std::max(1, env_int("ECSR_B200_PRE", 2)); }
+bool trace_enabled() { return env_int("ECSR_B200_TRACE", 0) != 0; }
+bool trace_caller_resets() { return env_int("ECSR_B200_TRACE", 0) == 2; }
+#else
+int tile_target() { return t_tile_override ? t_tile_override : g_tile_default; }
+int pre_tiles() { return 2; }  // tiles streamed before griddepcontrol.wait and the x copy
+constexpr bool trace_enabled() { return false; }
+constexpr bool trace_caller_resets() { return false; }
+#endif
 constexpr int kMaxStageBytes = 65536;   // largest tile a ring slot may hold
 constexpr int kMaxStages = 16;
 constexpr int kPackInternal = 1 << 30;  // spmv_set: unbounded u32 deltas (validated by range)
+constexpr double kQueueShare = 0.05;    // cost share of each CTA's range moved to the tail queue
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
@@ -195,18 +196,45 @@ struct ecsr_dev {
     int64_t arena_bytes = 0;
     uint32_t* d_tile_start16 = nullptr;
     int64_t ntiles = 0;
-    uint32_t* d_cta_tile = nullptr;
-    uint32_t* d_tile_rec = nullptr;        // [ntiles + 1] record prefix counts
-    unsigned long long* d_sync = nullptr;  // zero-y grid-barrier generation counter
+    uint32_t* d_cta_tile = nullptr;        // [2 * grid] static tile range of each CTA
+    uint32_t* d_tile_meta = nullptr;       // [2 * ntiles] {start16, nrec | bytes16 << 16}
+    uint32_t queue_begin = 0, nqueue = 0;  // the launch's tail-queue tiles
     bool lean = false;                     // every run uses a lean-kernel record variant
     int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
     std::vector<TileFeat> tile_feat;       // per tile (cost-model calibration)
     std::vector<uint32_t> cta_tile_h;      // host copy of the CTA tile boundaries
     std::vector<uint32_t> cta_range_h;     // per block [lo, hi) (launch order)
-    unsigned long long* d_trace = nullptr; // debug timeline (ECSR_B200_DEBUG & 4)
+    unsigned long long* d_trace = nullptr; // tuning builds: per-CTA timeline
     int grid = 0, stage_bytes = 0, nstages = 0, wide = 0, smem_bytes = 0;
+    // Per-stream launch workspaces: the zero-y gate's generation counter and the
+    // ordered mode's block partials are written by a launch, so two launches of one
+    // handle may overlap only if they use different ones. A handle binds up to
+    // kStreamSlots streams (first come) to its own workspace each; launches issued on
+    // (or captured from) one stream are stream-ordered, so they never share one
+    // concurrently. Allocated at pack time: nothing is allocated on the launch path
+    // (safe under CUDA graph capture).
+    struct Workspace {
+        unsigned long long* sync = nullptr;  // zero-y grid-gate generation counter (own 128-B line)
+        uint32_t* queue = nullptr;           // tail queue {next tile, CTAs done} (own 128-B line)
+        void* partials = nullptr;            // [nslots] ordered-mode block partials
+    };
+    static constexpr int kStreamSlots = 4;
+    Workspace ws[kStreamSlots];
+    mutable cudaStream_t ws_stream[kStreamSlots] = {};
+    mutable int ws_bound = 0;
+    mutable std::mutex ws_mu;
+
+    // The workspace of `stream` (bound on first use), or null when kStreamSlots other
+    // streams already hold one.
+    const Workspace* workspace(cudaStream_t stream) const {
+        std::lock_guard<std::mutex> lock(ws_mu);
+        for (int i = 0; i < ws_bound; ++i)
+            if (ws_stream[i] == stream) return &ws[i];
+        if (ws_bound == kStreamSlots) return nullptr;
+        ws_stream[ws_bound] = stream;
+        return &ws[ws_bound++];
+    }
     // ordered reduction
-    void* d_partials = nullptr;
     uint32_t* d_row_ptr = nullptr;
     uint32_t* d_row_slots = nullptr;
     // generic layout
@@ -333,14 +361,13 @@ constexpr int64_t kRecordCap = 24 * 1024;
 // A ring stage holds whole records, so records much larger than a tile leave consumer
 // warps without work (fewer resident records than warps): a run's AVERAGE record is
 // also held to ~rec_cap() = half a tile (ECSR_B200_RECCAP overrides, for tuning).
-int64_t rec_max() {  // hard record-size cap (ECSR_B200_RECMAX overrides, for tuning)
-    const char* e = std::getenv("ECSR_B200_RECMAX");
-    return e ? static_cast<int64_t>(std::max(512, std::atoi(e))) : kRecordCap;
-}
-int64_t rec_cap() {  // read at every pack (tuning sweeps change it between packs)
-    const char* e = std::getenv("ECSR_B200_RECCAP");
-    return e ? static_cast<int64_t>(std::max(512, std::atoi(e))) : tile_target() / 2;
-}
+#ifdef ECSR_B200_TUNING
+int64_t rec_max() { return std::max(512, env_int("ECSR_B200_RECMAX", static_cast<int>(kRecordCap))); }
+int64_t rec_cap() { return std::max(512, env_int("ECSR_B200_RECCAP", tile_target() / 2)); }
+#else
+int64_t rec_max() { return kRecordCap; }
+int64_t rec_cap() { return tile_target() / 2; }
+#endif
 
 int group_p(int g) { return g > 8 ? 1 : ecsr::group_blocks(g); }
 
@@ -578,10 +605,20 @@ int build_slots(ecsr_dev* d, const ecsr_host_set* sets, int nsets, int64_t* tota
     d->d_row_slots = dalloc_copy(slots, total, &err);
     if (d->d_row_slots) d->allocs.push_back(d->d_row_slots);
     ECSR_CUDA(err);
-    const size_t pbytes = std::max<size_t>(16, d->nslots * (d->dtype == ECSR_F64 ? 8 : 4));
-    ECSR_CUDA(cudaMalloc(&d->d_partials, pbytes));
-    d->allocs.push_back(d->d_partials);
-    *total += static_cast<int64_t>(pbytes);
+    const size_t pbytes = round_up(std::max<int64_t>(16, d->nslots * (d->dtype == ECSR_F64 ? 8 : 4)), 256);
+    uint8_t* part = nullptr;
+    ECSR_CUDA(cudaMalloc(&part, pbytes * ecsr_dev::kStreamSlots));
+    d->allocs.push_back(part);
+    unsigned long long* sync = nullptr;  // two 128-B lines per workspace: gate, queue
+    ECSR_CUDA(cudaMalloc(&sync, 256 * ecsr_dev::kStreamSlots));
+    d->allocs.push_back(sync);
+    ECSR_CUDA(cudaMemset(sync, 0, 256 * ecsr_dev::kStreamSlots));
+    for (int i = 0; i < ecsr_dev::kStreamSlots; ++i) {
+        d->ws[i].partials = part + pbytes * i;
+        d->ws[i].sync = sync + 32 * i;
+        d->ws[i].queue = reinterpret_cast<uint32_t*>(sync + 32 * i + 16);
+    }
+    *total += static_cast<int64_t>(pbytes * ecsr_dev::kStreamSlots + 256 * ecsr_dev::kStreamSlots);
     return ECSR_OK;
 }
 
@@ -658,11 +695,14 @@ void fill_model_bytes(ecsr_dev* d, const ecsr_host_set* sets, int nsets) {
                            b.block_values + 2 * d->K + 4 * d->M;
 }
 
-int configure_tiled_kernels(int smem) {
+// The dynamic shared-memory opt-in is a per-device (per-context) function attribute:
+// track the configured size per device index.
+int configure_tiled_kernels(int device, int smem) {
     static std::mutex mu;
-    static int configured = 0;
+    static std::vector<int> configured;
     std::lock_guard<std::mutex> lock(mu);
-    if (configured >= smem) return ECSR_OK;
+    if (device >= static_cast<int>(configured.size())) configured.resize(device + 1, 0);
+    if (configured[device] >= smem) return ECSR_OK;
     ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, 8>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, 8>,
@@ -671,9 +711,23 @@ int configure_tiled_kernels(int smem) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, 16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = smem;
+    configured[device] = smem;
     return ECSR_OK;
 }
+
+// Makes `device` current for the scope of a call and restores the caller's device.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int device) {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != device) err = cudaSetDevice(device);
+        else if (err == cudaSuccess) prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 template <typename K, typename... Args>
 cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
@@ -692,7 +746,8 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_
 }
 
 template <typename T, typename VT, typename XT>
-cudaError_t launch_generic_set(const ecsr_dev* d, const SetDesc& sd, const void* x, cudaStream_t st) {
+cudaError_t launch_generic_set(const ecsr_dev* d, const SetDesc& sd, const void* x, void* partials,
+                               cudaStream_t st) {
     ecsr::GenericSet gs;
     gs.base_indices = d->d_bases + sd.base_off;
     gs.block_indptr = d->d_indptr + sd.indptr_off;
@@ -709,7 +764,7 @@ cudaError_t launch_generic_set(const ecsr_dev* d, const SetDesc& sd, const void*
     const int warps_per_cta = 8;
     int64_t ctas = (sd.nb + warps_per_cta - 1) / warps_per_cta;
     ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 16));
-    T* part = static_cast<T*>(d->d_partials);
+    T* part = static_cast<T*>(partials);
     const XT* xx = static_cast<const XT*>(x);
     dim3 grid(static_cast<unsigned>(ctas)), block(32 * warps_per_cta);
     if (sd.g <= 1) return launch_pdl(ecsr::ecsr_generic_kernel<T, VT, XT, 1>, grid, block, 0, st, gs, xx, part);
@@ -720,14 +775,14 @@ cudaError_t launch_generic_set(const ecsr_dev* d, const SetDesc& sd, const void*
 }
 
 template <typename T>
-cudaError_t launch_finish(const ecsr_dev* d, void* y, int accumulate, cudaStream_t st) {
+cudaError_t launch_finish(const ecsr_dev* d, void* y, int accumulate, const void* partials, cudaStream_t st) {
     const int threads = 256;
     int64_t ctas = (d->M + threads - 1) / threads;
     ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, 148 * 8));
     return launch_pdl(ecsr::ecsr_finish_rows<T>, dim3(static_cast<unsigned>(ctas)), dim3(threads), 0,
                       st, static_cast<const uint32_t*>(d->d_row_ptr),
                       static_cast<const uint32_t*>(d->d_row_slots),
-                      static_cast<const T*>(d->d_partials), static_cast<T*>(y), d->M, accumulate);
+                      static_cast<const T*>(partials), static_cast<T*>(y), d->M, accumulate);
 }
 
 }  // namespace
@@ -825,6 +880,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
     if (tiled) {
         static std::mutex tile_mu;  // the packer is host code; serialise the tile default
         std::lock_guard<std::mutex> lock(tile_mu);
+        t_tile_override = ((flags >> 8) & 0xff) * 1024;  // 0: the default
         // The stage pool fills the CTA's shared memory: stages of ~16 KB (2 CTAs/SM) or
         // ~32 KB (1 CTA), stretched so that a whole number of them uses all of it
         // (more bytes in flight per SM; e.g. 5 x 18.3 KB instead of 5 x 16 KB at K = 8192).
@@ -873,20 +929,35 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             // cost-balanced contiguous tile ranges (fitted consumer-time model)
             const std::vector<uint32_t> cta = balanced_ranges(tcost, grid);
             // Within each CTA's range, tiles go longest record first (LPT): records are
-            // handed to warps in arena order, so the last ones of a CTA are short and the
-            // launch's tail shrinks. Unpack identifies blocks by slot, not position.
+            // handed to warps in issue order, so the last ones of a CTA are short. The
+            // cheapest end of every range (cost share `qshare`) moves to the launch's tail
+            // queue, most expensive tile first, drawn by whichever CTAs run ahead of the
+            // cost model. Unpack identifies blocks by slot, not position.
+            const double qshare = (flags & (0x80 << 16)) ? ((flags >> 16) & 0x7f) / 100.0 : kQueueShare;
+            std::vector<uint32_t> order, scta(grid + 1, 0), qtiles;
+            order.reserve(ntiles);
+            for (int c2 = 0; c2 < grid; ++c2) {
+                std::vector<uint32_t> ts;
+                for (uint32_t t = cta[c2]; t < cta[c2 + 1]; ++t) ts.push_back(t);
+                std::stable_sort(ts.begin(), ts.end(), [&](uint32_t x, uint32_t y) {
+                    const double cx = tcost[x] / std::max<uint32_t>(1, trec[x + 1] - trec[x]);
+                    const double cy = tcost[y] / std::max<uint32_t>(1, trec[y + 1] - trec[y]);
+                    return cx > cy;
+                });
+                double rcost = 0, moved = 0;
+                for (uint32_t t : ts) rcost += tcost[t];
+                size_t keep = ts.size();
+                while (keep > 1 && moved + tcost[ts[keep - 1]] <= qshare * rcost) moved += tcost[ts[--keep]];
+                scta[c2] = static_cast<uint32_t>(order.size());
+                order.insert(order.end(), ts.begin(), ts.begin() + keep);
+                qtiles.insert(qtiles.end(), ts.begin() + keep, ts.end());
+            }
+            scta[grid] = static_cast<uint32_t>(order.size());
+            std::stable_sort(qtiles.begin(), qtiles.end(), [&](uint32_t x, uint32_t y) { return tcost[x] > tcost[y]; });
+            d->queue_begin = static_cast<uint32_t>(order.size());
+            d->nqueue = static_cast<uint32_t>(qtiles.size());
+            order.insert(order.end(), qtiles.begin(), qtiles.end());
             {
-                std::vector<uint32_t> order(ntiles);
-                for (int c2 = 0; c2 < grid; ++c2) {
-                    std::vector<uint32_t> ts;
-                    for (uint32_t t = cta[c2]; t < cta[c2 + 1]; ++t) ts.push_back(t);
-                    std::stable_sort(ts.begin(), ts.end(), [&](uint32_t x, uint32_t y) {
-                        const double cx = tcost[x] / std::max<uint32_t>(1, trec[x + 1] - trec[x]);
-                        const double cy = tcost[y] / std::max<uint32_t>(1, trec[y + 1] - trec[y]);
-                        return cx > cy;
-                    });
-                    std::copy(ts.begin(), ts.end(), order.begin() + cta[c2]);
-                }
                 std::vector<uint8_t> na;
                 na.reserve(arena.size());
                 std::vector<uint32_t> nts(ntiles + 1), ntr(ntiles + 1, 0);
@@ -907,6 +978,12 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 tcost.swap(ntc);
                 d->tile_feat.swap(ntf);
             }
+            // per tile {start16, nrec | bytes16 << 16} (a tile is at most 64 KB)
+            std::vector<uint32_t> meta(2 * std::max<int64_t>(ntiles, 1), 0u);
+            for (int64_t t = 0; t < ntiles; ++t) {
+                meta[2 * t] = tstart[t];
+                meta[2 * t + 1] = (trec[t + 1] - trec[t]) | ((tstart[t + 1] - tstart[t]) << 16);
+            }
             cudaError_t err = cudaSuccess;
             d->arena_bytes = static_cast<int64_t>(arena.size());
             d->d_arena = dalloc_copy(arena, &total, &err);
@@ -915,31 +992,27 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 d->d_tile_start16 = dalloc_copy(tstart, &total, &err);
                 if (d->d_tile_start16) d->allocs.push_back(d->d_tile_start16);
             }
-            d->cta_tile_h = cta;
+            if (err == cudaSuccess) {
+                d->d_tile_meta = dalloc_copy(meta, &total, &err);
+                if (d->d_tile_meta) d->allocs.push_back(d->d_tile_meta);
+            }
+            d->cta_tile_h = scta;
             std::vector<uint32_t> ranges(2 * grid);
             for (int b = 0; b < grid; ++b) {
                 const int r = range_of_block(b, grid, ctas_per_sm);
-                ranges[2 * b] = cta[r];
-                ranges[2 * b + 1] = cta[r + 1];
+                ranges[2 * b] = scta[r];
+                ranges[2 * b + 1] = scta[r + 1];
             }
             d->cta_range_h = ranges;
             if (err == cudaSuccess) {
                 d->d_cta_tile = dalloc_copy(ranges, &total, &err);
                 if (d->d_cta_tile) d->allocs.push_back(d->d_cta_tile);
             }
-            if (err == cudaSuccess) {
-                d->d_tile_rec = dalloc_copy(trec, &total, &err);
-                if (d->d_tile_rec) d->allocs.push_back(d->d_tile_rec);
-            }
-            if (err == cudaSuccess) {
-                d->d_sync = dalloc_copy(std::vector<unsigned long long>(2, 0ull), &total, &err);
-                if (d->d_sync) d->allocs.push_back(d->d_sync);
-            }
             if (err != cudaSuccess) {
                 delete d;
                 return fail(ECSR_ERR_CUDA, std::string("tiled upload: ") + cudaGetErrorString(err));
             }
-            rc = configure_tiled_kernels(d->smem_bytes);
+            rc = configure_tiled_kernels(dev, d->smem_bytes);
             if (rc) {
                 delete d;
                 return rc;
@@ -956,6 +1029,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             return rc;
         }
     }
+    t_tile_override = 0;
     rc = build_slots(d, sets, nsets, &total);
     if (rc) {
         delete d;
@@ -968,6 +1042,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
     d->bytes.stages = d->nstages;
     d->bytes.stage_bytes = d->stage_bytes;
     d->bytes.tiles = d->ntiles;
+    d->bytes.queue_tiles = d->nqueue;
     *out = d;
     return ECSR_OK;
 }
@@ -979,33 +1054,40 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
     const int accumulate = mode & ECSR_SPMV_ACCUMULATE;
     const bool ordered = (mode & ECSR_SPMV_ORDERED) != 0 || d->layout == 2;
     if (d->M == 0) return ECSR_OK;
+    const ecsr_dev::Workspace* ws = d->workspace(st);
+    if (!ws)
+        return fail(ECSR_ERR_VALUE, "handle already used from " + std::to_string(ecsr_dev::kStreamSlots) +
+                                        " other streams (one workspace per stream)");
+    DeviceGuard guard(d->device);  // the handle's device, whatever the caller's current one
+    ECSR_CUDA(guard.err);
     if (d->layout == 1) {
         ecsr::TiledParams p;
         p.arena = d->d_arena;
-        p.tile_start16 = d->d_tile_start16;
+        p.tile_meta = reinterpret_cast<const uint2*>(d->d_tile_meta);
         p.cta_tile = d->d_cta_tile;
-        p.tile_rec = d->d_tile_rec;
+        p.queue = ws->queue;
+        p.queue_begin = d->queue_begin;
+        p.nqueue = d->nqueue;
         p.x = static_cast<const __half*>(x);
         p.y = static_cast<float*>(y);
-        p.partials = static_cast<float*>(d->d_partials);
+        p.partials = static_cast<float*>(ws->partials);
         p.K = static_cast<int32_t>(d->K);
         p.ordered = ordered ? 1 : 0;
         p.stage_bytes = d->stage_bytes;
         p.nstages = d->nstages;
         p.x_vec16 = (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-        p.debug = debug_flags();
         p.pre_tiles = std::min(pre_tiles(), std::max(1, d->nstages - 1));
-        p.sync = d->d_sync;
+        p.sync = ws->sync;
         p.M = d->M;
         p.zero_y = (!ordered && !accumulate) ? 1 : 0;
         p.trace = nullptr;
-        if (debug_flags() & 4) {
+        if (trace_enabled()) {  // tuning builds only
             ecsr_dev* dm = const_cast<ecsr_dev*>(d);
             if (!dm->d_trace) {
                 ECSR_CUDA(cudaMalloc(&dm->d_trace, 8 * 16 * d->grid));
                 dm->allocs.push_back(dm->d_trace);
             }
-            if (!(debug_flags() & 8)) {  // 8: the caller resets (back-to-back traced launches)
+            if (!trace_caller_resets()) {
                 std::vector<unsigned long long> init(16 * d->grid, 0ull);
                 for (int c = 0; c < d->grid; ++c) init[16 * c + 7] = ~0ull;
                 ECSR_CUDA(cudaMemcpyAsync(dm->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice, st));
@@ -1024,19 +1106,19 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
             e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false, 16>, grd, blk, d->smem_bytes, st, p)
                         : launch_pdl(ecsr::ecsr_tiled_kernel<true, 16>, grd, blk, d->smem_bytes, st, p);
         ECSR_CUDA(e);
-        if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
+        if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, ws->partials, st));
         return ECSR_OK;
     }
     for (const SetDesc& sd : d->sets) {
         if (sd.nb == 0) continue;
         cudaError_t e;
-        if (d->dtype == ECSR_F16) e = launch_generic_set<float, __half, __half>(d, sd, x, st);
-        else if (d->dtype == ECSR_F32) e = launch_generic_set<float, float, float>(d, sd, x, st);
-        else e = launch_generic_set<double, double, double>(d, sd, x, st);
+        if (d->dtype == ECSR_F16) e = launch_generic_set<float, __half, __half>(d, sd, x, ws->partials, st);
+        else if (d->dtype == ECSR_F32) e = launch_generic_set<float, float, float>(d, sd, x, ws->partials, st);
+        else e = launch_generic_set<double, double, double>(d, sd, x, ws->partials, st);
         ECSR_CUDA(e);
     }
-    if (d->dtype == ECSR_F64) ECSR_CUDA(launch_finish<double>(d, y, accumulate, st));
-    else ECSR_CUDA(launch_finish<float>(d, y, accumulate, st));
+    if (d->dtype == ECSR_F64) ECSR_CUDA(launch_finish<double>(d, y, accumulate, ws->partials, st));
+    else ECSR_CUDA(launch_finish<float>(d, y, accumulate, ws->partials, st));
     return ECSR_OK;
 }
 

@@ -41,13 +41,15 @@ namespace ecsr {
 constexpr int kConsumerWarpsPerSm = 16;
 __host__ __device__ constexpr int tiled_threads(int nc) { return 32 * (nc + 1); }
 constexpr int kMaxRingStages = 16;
-constexpr uint32_t kTileRecCache = 256;  // per-CTA record prefix counts kept in smem
+constexpr int kTickets = 3;  // tail-queue tickets a producer keeps in flight
 
 struct TiledParams {
     const uint8_t* arena;          // block-major tiles, 16-B aligned
-    const uint32_t* tile_start16;  // [ntiles + 1] tile offsets in 16-B units
-    const uint32_t* cta_tile;      // [2 * grid] tile range [lo, hi) of each CTA
-    const uint32_t* tile_rec;      // [ntiles + 1] record prefix counts
+    const uint2* tile_meta;        // [ntiles] {start16, nrec | bytes16 << 16}
+    const uint32_t* cta_tile;      // [2 * grid] static tile range [lo, hi) of each CTA
+    uint32_t* queue;               // [2] tail queue {next tile, CTAs done} (per-stream workspace)
+    uint32_t queue_begin;          // tiles [queue_begin, queue_begin + nqueue) go through the queue
+    uint32_t nqueue;
     const __half* x;               // [K]
     float* y;                      // [M]
     float* partials;               // [nslots] (ordered mode)
@@ -60,9 +62,8 @@ struct TiledParams {
     int32_t x_vec16;               // x is 16-B aligned
     int32_t zero_y;                // overwrite: the kernel zeroes y itself (no memset launch)
     int32_t wide;                  // K > 65535: u32 bases (else u16)
-    int32_t debug;                 // tuning experiments (ECSR_B200_DEBUG)
     int32_t pre_tiles;             // tiles streamed before griddepcontrol.wait / x
-    unsigned long long* trace;     // debug timeline [grid][8] (globaltimer ns) or null
+    unsigned long long* trace;     // tuning builds: per-CTA timeline [grid][16] or null
 };
 
 // ---------------------------------------------------------------------------------
@@ -86,16 +87,21 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Returns 0 through an asm output: add it to addresses of data the wait guards.
+__device__ __forceinline__ uint32_t mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t token;
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
         "@P1 bra DONE_%=;\n\t"
         "bra WAIT_%=;\n"
-        "DONE_%=:\n\t}" ::"r"(smem_addr(bar)),
-        "r"(parity)
+        "DONE_%=:\n\t"
+        "mov.u32 %0, 0;\n\t}"
+        : "=r"(token)
+        : "r"(smem_addr(bar)), "r"(parity)
         : "memory");
+    return token;
 }
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     uint64_t pol;
@@ -161,6 +167,10 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&acc)[G], int lane) 
 }
 
 // Load `Bytes` (power of two) from shared memory (32-bit shared address) into regs.
+// These asm statements have no memory operands the compiler can see, so nothing but
+// data dependences orders them: every address into a stage or into x is derived from
+// the token of the mbarrier wait that completes its fill (mbar_wait returns 0 through
+// an asm output), so no load can be scheduled above that wait.
 template <int Bytes>
 __device__ __forceinline__ void lds_bytes(uint32_t addr, uint32_t* r) {
     if constexpr (Bytes >= 16) {
@@ -505,17 +515,23 @@ __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P
 }
 
 // Persistent grid (1 or 2 CTAs per SM, kConsumerWarpsPerSm above), warp-specialised:
-//   * producer warp: streams this CTA's tile range HBM -> shared memory with
-//     cp.async.bulk into the stage pool, L2 evict_first; the first tiles go out before
-//     griddepcontrol.wait because the weights never depend on the previous kernel (PDL
-//     overlap of weight streaming with the predecessor's tail);
+//   * producer warp: streams this CTA's tiles HBM -> shared memory with cp.async.bulk
+//     into the stage pool, L2 evict_first: first its static tile range (the first tiles
+//     before griddepcontrol.wait -- the weights never depend on the previous kernel, so
+//     they stream under the predecessor's tail), then tiles from the launch's tail queue
+//     until it is empty. The queue (the cheapest ~5 % of the work, most expensive
+//     first) goes to whichever CTAs run ahead, so the launch's CTAs finish together: the
+//     static split alone leaves a +-12 % spread of per-CTA times (HBM and SM variation a
+//     cost model cannot see), i.e. a ~3 us tail per launch;
 //   * consumer warps: wait for the predecessor (x producer) and for x in shared
-//     memory, then decode records from the pool.
+//     memory, then take records in issue order from a shared counter.
 // Overwrite without a memset launch (zero_y): every CTA zeroes its slice of y, then
 // bumps a 64-bit generation counter; warps pass the gate (counter reached the
 // generation's multiple of gridDim.x) before their first red.global. PDL dependents
 // are released only after the arrival, so back-to-back launches of one handle never
-// interleave their generations.
+// interleave their generations. The queue counter is reset by the launch's last CTA
+// once every CTA has drawn its last (failing) ticket; the next launch on the stream
+// draws only after its griddepcontrol.wait, i.e. after that reset.
 template <bool kFull, int NC>
 __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
@@ -528,20 +544,22 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     __half* xs = reinterpret_cast<__half*>(stages + p.nstages * p.stage_bytes);
     __shared__ unsigned long long gate_target;
     __shared__ uint32_t gate_state;                 // 0 closed, 1 a warp polls, 2 open
-    __shared__ uint32_t rec_next;                   // dynamic record scheduler
-    __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per ring stage
+    __shared__ uint32_t rec_next;                   // record claim counter
+    __shared__ uint32_t final_rec;                  // records of all issued tiles, once final
+    __shared__ uint32_t stage_done[kMaxRingStages];  // finished records per stage
     // The stages form a pool, not an in-order ring: the producer refills whichever stage
-    // was released (a long record then holds one stage, not the whole ring). Before the
-    // copy it publishes (tile, stage, parity of this fill of the stage's full barrier) in
-    // the tile -> stage map; consumers look their tile up there and wait on that parity.
-    __shared__ uint32_t tile_rec_s[kTileRecCache];
-    // tile -> stage map (ring of 32 > kMaxRingStages tiles in flight): entry
-    // (tile << 6 | stage << 1 | parity), written by the producer at issue
-    __shared__ uint32_t tile_stage[32];
+    // was released (a long record then holds one stage, not the whole pool). At issue it
+    // publishes, for the CTA's li-th tile, the records of tiles [0, li] and then (li,
+    // stage, parity of this fill of the stage's full barrier); consumers find the tile
+    // of their record there and wait on that parity. A ring of 32 > kMaxRingStages
+    // entries: a tile's entry is reused only after 16 later tiles were fully consumed.
+    // entry: low word (li << 6 | stage << 1 | parity), high word records of tiles [0, li];
+    // one 64-bit store / load, so a consumer never sees half an entry
+    __shared__ unsigned long long tile_stage[32];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t t0 = p.cta_tile[2 * blockIdx.x];      // [t0, t1): this CTA's tiles
+    const uint32_t t0 = p.cta_tile[2 * blockIdx.x];  // [t0, t1): this CTA's static tiles
     const uint32_t t1 = p.cta_tile[2 * blockIdx.x + 1];
     // x by one bulk copy when it is 16-B aligned and a multiple of 16 bytes
     const bool x_bulk = p.x_vec16 && (p.K & 7) == 0 && p.K > 0;
@@ -551,9 +569,10 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             mbar_init(&full[s], 1);
             stage_done[s] = 0;
         }
-        for (int i = 0; i < 32; ++i) tile_stage[i] = 0xffffffffu;
+        for (int i = 0; i < 32; ++i) tile_stage[i] = 0xffffffffull;
         mbar_init(xbar, 1);
         rec_next = 0;
+        final_rec = 0xffffffffu;
         gate_target = 0;
         gate_state = 0;
         fence_mbar_init();
@@ -568,22 +587,18 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
 
     if (warp == kProducerWarp) {
         // The whole warp runs the producer loop: lanes < nstages poll the stage pool in
-        // parallel (ballot), lane 0 issues the copies. One tile goes out before x: it
-        // never depends on the predecessor kernel; the rest waits until x has landed,
-        // so the x request is not queued behind this SM's whole weight stream.
+        // parallel (ballot), lane 0 issues the copies. `pre_tiles` tiles go out before
+        // x; the rest waits until x has landed, so the x request is not queued behind
+        // this SM's whole weight stream.
         if (!p.zero_y) pdl_trigger();
         const uint64_t policy = l2_evict_first_policy();
         uint32_t fill_parity = 0;  // bit s: parity of the next fill of stage s
-        uint32_t t = t0;
-        // lane s < nstages: records of the tile in stage s (0 = empty). A stage is free
-        // once the consumers' done count (a shared red, no return value on their side)
-        // reaches it.
+        uint32_t li = 0;           // tiles issued by this CTA (static, then queue tiles)
+        uint32_t rec_end = 0;      // records of the issued tiles
+        // lane s < nstages: records of the tile in stage s. A stage is free once the
+        // consumers' done count (a shared red, no return value on their side) reaches it.
         uint32_t expect = 0;
-        // record prefix counts of tiles [win_base, win_base + 32) in the lanes (one
-        // coalesced load per 31 tiles, no global round trip per issue)
-        uint32_t win_base = t0;
-        uint32_t win = t0 + lane <= t1 ? p.tile_rec[t0 + lane] : 0u;
-        auto issue = [&]() {
+        auto issue_tile = [&](uint32_t a16, uint32_t info) {  // info: nrec | bytes16 << 16
             uint32_t freeset;
             while (true) {
                 uint32_t f = 0;
@@ -597,34 +612,42 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
                 __nanosleep(20);
             }
             const int stage = __ffs(freeset) - 1;
-            if (t + 1 - win_base >= 32u) {  // warp-uniform window slide
-                win_base = t;
-                win = t + lane <= t1 ? p.tile_rec[t + lane] : 0u;
-            }
-            const uint32_t nrec = __shfl_sync(0xffffffffu, win, t + 1 - win_base) -
-                                  __shfl_sync(0xffffffffu, win, t - win_base);
+            const uint32_t nrec = info & 0xffffu;
             if (lane == stage) expect = nrec;
+            rec_end += nrec;
             if (lane == 0) {
                 stage_done[stage] = 0;
                 // generic-proxy reads of the old tile are complete (their values were
                 // consumed); order them before the async-proxy overwrite
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 const uint32_t par = (fill_parity >> stage) & 1u;
-                const uint32_t a = p.tile_start16[t], b = p.tile_start16[t + 1];
-                const uint32_t bytes = (b - a) * 16u;
-                asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&tile_stage[(t - t0) & 31u])),
-                             "r"(((t - t0) << 6) | (static_cast<uint32_t>(stage) << 1) | par)
+                const uint32_t bytes = (info >> 16) * 16u;
+                asm volatile("st.volatile.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_addr(&tile_stage[li & 31u])),
+                             "r"((li << 6) | (static_cast<uint32_t>(stage) << 1) | par), "r"(rec_end)
                              : "memory");
                 mbar_arrive_expect_tx(&full[stage], bytes);
-                bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a) * 16u, bytes,
+                bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a16) * 16u, bytes,
                          &full[stage], policy);
             }
             fill_parity ^= 1u << stage;
-            ++t;
+            ++li;
             __syncwarp();
         };
-        for (int k = 0; k < p.pre_tiles && t < t1; ++k) issue();
-        if (x_bulk || p.zero_y) pdl_wait();
+        // static tiles: their metadata rides in the lanes, 32 tiles per coalesced load
+        uint32_t t = t0, win_base = t0;
+        uint2 win = t0 + lane < t1 ? p.tile_meta[t0 + lane] : make_uint2(0u, 0u);
+        auto issue_static = [&]() {
+            if (t - win_base >= 32u) {  // warp-uniform window slide
+                win_base = t;
+                win = t + lane < t1 ? p.tile_meta[t + lane] : make_uint2(0u, 0u);
+            }
+            const uint32_t a16 = __shfl_sync(0xffffffffu, win.x, t - win_base);
+            const uint32_t info = __shfl_sync(0xffffffffu, win.y, t - win_base);
+            issue_tile(a16, info);
+            ++t;
+        };
+        for (int k = 0; k < p.pre_tiles && t < t1; ++k) issue_static();
+        if (x_bulk || p.zero_y || p.nqueue) pdl_wait();
         if (x_bulk && lane == 0) {
             const uint32_t xbytes = static_cast<uint32_t>(p.K) * 2u;
             mbar_arrive_expect_tx(xbar, xbytes);
@@ -650,43 +673,66 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             __syncwarp();
         }
         mbar_wait(xbar, 0);
-        while (t < t1) issue();
+        while (t < t1) issue_static();
+        if (p.nqueue) {
+            // Tail queue: lanes 0..kTickets-1 each hold one drawn ticket and its tile's
+            // metadata, so ticket and metadata latencies (~1 us each) overlap each other
+            // and the wait for free stages; an exhausted lane stops drawing.
+            uint32_t tk = 0xffffffffu;
+            uint2 meta = make_uint2(0u, 0u);
+            if (lane < kTickets) {
+                tk = atomicAdd(p.queue, 1u);
+                if (tk < p.nqueue) meta = p.tile_meta[p.queue_begin + tk];
+            }
+            int head = 0;
+            while (true) {
+                const uint32_t valid = __ballot_sync(0xffffffffu, tk < p.nqueue);
+                if (!valid) break;
+                // the next valid lane at or after head (round robin)
+                const uint32_t rot = (valid >> head) | (valid << ((32 - head) & 31));
+                const int src = (head + __ffs(rot) - 1) & 31;
+                issue_tile(__shfl_sync(0xffffffffu, meta.x, src), __shfl_sync(0xffffffffu, meta.y, src));
+                if (lane == src) {
+                    tk = atomicAdd(p.queue, 1u);
+                    if (tk < p.nqueue) meta = p.tile_meta[p.queue_begin + tk];
+                }
+                head = (src + 1) % kTickets;
+            }
+            // every ticket this CTA drew has landed (its value was used): check out; the
+            // last CTA out resets the queue for the next launch on this workspace
+            if (lane == 0) {
+                const uint32_t out = atomicAdd(p.queue + 1, 1u);
+                if (out == gridDim.x - 1) {
+                    p.queue[0] = 0u;
+                    p.queue[1] = 0u;
+                }
+            }
+        }
+        if (lane == 0)  // after the last tile's entry: consumers past it may exit
+            asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(&final_rec)), "r"(rec_end) : "memory");
         ECSR_TRACE(5, lane == 0);
         return;
     }
 
-    // Consumers. The record prefix counts of this CTA's tiles are cached in shared
-    // memory first: they never depend on the previous kernel, so these loads overlap
-    // the wait for the predecessor and for x.
+    // Consumers: wait for the predecessor (x producer; y may alias its inputs), then x.
     const int tid = threadIdx.x;
     constexpr int nthr = NC * 32;
-    const uint32_t rec0 = p.tile_rec[t0];
-    const uint32_t nrec_cta = p.tile_rec[t1] - rec0;
-    const uint32_t ntl = t1 - t0;
-    for (uint32_t i = tid; i <= ntl && i < kTileRecCache; i += nthr) tile_rec_s[i] = p.tile_rec[t0 + i] - rec0;
-    // wait for the predecessor (x producer; y may alias its inputs)
     pdl_wait();
     ECSR_TRACE(1, threadIdx.x == 0);
-
-    if (!x_bulk)
+    if (!x_bulk) {
         for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
-    consumer_bar_sync<NC>();  // tile_rec_s (and a consumer-copied x) complete
-    if (!x_bulk && tid == 0) mbar_arrive(xbar);
+        consumer_bar_sync<NC>();
+        if (tid == 0) mbar_arrive(xbar);
+    }
     YGate gate{p.sync, &gate_target, &gate_state, !p.zero_y};
-    mbar_wait(xbar, 0);
+    const uint32_t xs_addr = smem_addr(xs) + mbar_wait(xbar, 0);  // x gathers after x landed
     ECSR_TRACE(2, threadIdx.x == 0);
 
-    const uint32_t xs_addr = smem_addr(xs);
     const uint32_t stages_addr = smem_addr(stages);
-    // Dynamic scheduling: warps take the CTA's records in container order from a
-    // shared counter (balances unequal records); the last warp to finish a tile's
-    // records releases its ring stage to the producer.
-    auto tile_rec_at = [&](uint32_t i) -> uint32_t {
-        return i < kTileRecCache ? tile_rec_s[i] : p.tile_rec[t0 + i] - rec0;
-    };
-    uint32_t ti = 0;                       // tile cursor (relative to t0)
-    uint32_t tile_end = tile_rec_at(1);
-    uint32_t tile_begin = 0;
+    // Warps claim records in issue order from a shared counter (balances unequal
+    // records); the last record of a tile to finish releases its stage to the producer.
+    uint32_t ti = 0;          // this warp's tile cursor (issue order)
+    uint32_t tile_begin = 0;  // records of tiles [0, ti)
 #ifdef ECSR_TRACE_CYCLES
     unsigned long long cyc_wait = 0, cyc_work = 0, nwork = 0, cyc_unissued = 0;
 #endif
@@ -694,42 +740,48 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         uint32_t k = 0;
         if (lane == 0) k = atomicAdd(&rec_next, 1u);
         k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= nrec_cta) break;
-        while (k >= tile_end) {
-            ++ti;
-            tile_begin = tile_end;
-            tile_end = tile_rec_at(ti + 1);
-        }
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c0 = clock64();
 #endif
-        uint32_t stage, par;
-        while (true) {  // the stage holding tile ti (tile -> stage map, one broadcast load)
-            uint32_t e;
-            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(e) : "r"(smem_addr(&tile_stage[ti & 31u])) : "memory");
-            if ((e >> 6) == ti) {
-                stage = (e >> 1) & 31u;
-                par = e & 1u;
-                break;
+        uint32_t stage = 0, par = 0;
+        bool have = false;
+        while (true) {  // the tile holding record k: walk the issued tiles' entries
+            uint32_t e, end;
+            asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e), "=r"(end)
+                         : "r"(smem_addr(&tile_stage[ti & 31u])) : "memory");
+            if ((e >> 6) == ti && e != 0xffffffffu) {
+                if (k < end) {
+                    stage = (e >> 1) & 31u;
+                    par = e & 1u;
+                    have = true;
+                    break;
+                }
+                tile_begin = end;
+                ++ti;
+                continue;
             }
+            uint32_t fin;  // not issued (yet): past the CTA's last record?
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(fin) : "r"(smem_addr(&final_rec)) : "memory");
+            if (k >= fin) break;
             __nanosleep(64);
         }
+        if (!have) break;
 #ifdef ECSR_TRACE_CYCLES
         cyc_unissued += clock64() - c0;  // the tile was not issued yet (no free stage)
 #endif
-        mbar_wait(&full[stage], par);
+        const uint32_t tok = mbar_wait(&full[stage], par);
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c1 = clock64();
         cyc_wait += c1 - c0;
 #endif
         ECSR_TRACE(3, threadIdx.x == 0 && ti == 0);
-        const uint32_t tile = stages_addr + stage * p.stage_bytes;
+        const uint32_t tile = stages_addr + stage * p.stage_bytes + tok;  // reads after the fill
         uint32_t th[2];
         lds_bytes<8>(tile, th);
         const uint32_t gv = th[1] & 0xffffu;
         uint32_t off16;
         lds_bytes<2>(tile + 8 + 2 * (k - tile_begin), &off16);
-        if (!(p.debug & 1)) tiled_record<kFull>(tile + 16u * off16, gv, th[1] >> 16, xs_addr, lane, p, gate);
+        tiled_record<kFull>(tile + 16u * (off16 & 0xffffu), gv, th[1] >> 16, xs_addr, lane, p, gate);
 #ifdef ECSR_TRACE_CYCLES
         cyc_work += clock64() - c1;
         ++nwork;

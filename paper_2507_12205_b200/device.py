@@ -52,7 +52,13 @@ def _host_sets(ec, check_shapes: bool = True):
 
 
 class DeviceMatrix:
-    """Opaque handle to a packed container (immutable after pack)."""
+    """Opaque handle to a packed container.
+
+    The packed layout is read-only after pack. Each launch also writes a small
+    workspace (the overwrite mode's grid-gate counter, the ordered mode's block
+    partials); the handle keeps one per CUDA stream (up to 4 streams), so launches
+    from different streams may overlap, and launches from one stream are ordered.
+    """
 
     def __init__(self, handle: int, num_rows: int, num_cols: int, device_dtype: str,
                  device_index: int):
@@ -106,9 +112,11 @@ class DeviceMatrix:
 
 
 def to_device(ec, device_dtype: str = "f16", force_generic: bool = False,
-              device=None) -> DeviceMatrix:
+              device=None, tile_kb: int | None = None, queue_pct: int | None = None) -> DeviceMatrix:
     """Validate once and upload (replaces the per-call `validate_container`,
-    `executor.py:85-86`). Raises ContainerError exactly where the reference would."""
+    `executor.py:85-86`). Raises ContainerError exactly where the reference would.
+    Tiled-layout options: `tile_kb` overrides the tile size (1..64 KB), `queue_pct` the
+    cost share (0..100 %) of each CTA's tiles drawn from the launch's tail queue."""
     torch = _torch()
     if device_dtype not in _DEVICE_DTYPES:
         raise ValueError(f"device_dtype must be one of {sorted(_DEVICE_DTYPES)}")
@@ -117,6 +125,14 @@ def to_device(ec, device_dtype: str = "f16", force_generic: bool = False,
     arr, keep, dtype = _host_sets(ec)
     out = ctypes.c_void_p()
     flags = _lib.PACK_FORCE_GENERIC if force_generic else _lib.PACK_DEFAULT
+    if tile_kb is not None:
+        if not 1 <= int(tile_kb) <= 64:
+            raise ValueError("tile_kb must be in [1, 64]")
+        flags |= int(tile_kb) << 8
+    if queue_pct is not None:
+        if not 0 <= int(queue_pct) <= 100:
+            raise ValueError("queue_pct must be in [0, 100]")
+        flags |= ((int(queue_pct) & 0x7F) | 0x80) << 16
     with torch.cuda.device(index):
         rc = _lib.lib().ecsr_b200_pack(arr, len(ec.sets), int(ec.num_rows), int(ec.num_cols),
                                        int(ec.warp_size), int(ec.delta_bits), int(ec.value_bits),
@@ -181,6 +197,8 @@ def spmv(W: DeviceMatrix, x, y=None, accumulate: bool = False, ordered: bool = F
         raise ValueError(f"x has shape {tuple(x.shape)}, expected ({W.num_cols},)")
     if x.dtype != W.x_dtype:
         raise ValueError(f"x must be {W.x_dtype}, got {x.dtype}")
+    if x.device.index != W.device_index:
+        raise ValueError(f"x is on cuda:{x.device.index}, the matrix on cuda:{W.device_index}")
     x = x.contiguous()
     if y is None:
         y = torch.empty(W.num_rows, dtype=W.y_dtype, device=x.device)
@@ -188,6 +206,8 @@ def spmv(W: DeviceMatrix, x, y=None, accumulate: bool = False, ordered: bool = F
             y.zero_()
     elif y.shape != (W.num_rows,) or y.dtype != W.y_dtype or not y.is_contiguous():
         raise ValueError("y must be a contiguous device tensor of shape (num_rows,) and y dtype")
+    elif not y.is_cuda or y.device.index != W.device_index:
+        raise ValueError(f"y must be on cuda:{W.device_index}")
     mode = (_lib.SPMV_ACCUMULATE if accumulate else _lib.SPMV_OVERWRITE) | (
         _lib.SPMV_ORDERED if ordered else 0)
     s = stream if stream is not None else torch.cuda.current_stream(x.device)

@@ -15,20 +15,21 @@ lib.ecsr_b200_debug_trace.restype = ctypes.c_int32
 lib.ecsr_b200_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
 lib.ecsr_b200_debug_trace_reset.restype = ctypes.c_int32
 lib.ecsr_b200_debug_trace_reset.argtypes = [ctypes.c_void_p]
-ecs, _ = bench.load_workload()
+LAUNCHES = bench.WORKLOADS[bench.HEADLINE]["launches"]
+ecs, _ = bench.load_workload(bench.HEADLINE)
 Ws, xs, ys = {}, {}, {}
-for ln, names in bench.LAUNCHES:
-    Ws[ln] = to_device(vstack([ecs[n] for n in names]))
+for ln, names in LAUNCHES:
+    Ws[ln] = to_device(vstack([ecs[n] for n in names]), queue_pct=QPCT)
     xs[ln] = torch.randn(Ws[ln].num_cols, device="cuda").half()
     ys[ln] = torch.empty(Ws[ln].num_rows, device="cuda")
 for _ in range(3):
-    for ln, _ in bench.LAUNCHES:
+    for ln, _ in LAUNCHES:
         spmv(Ws[ln], xs[ln], y=ys[ln])
 torch.cuda.synchronize()
 stream = torch.cuda.Stream()
 graph = torch.cuda.CUDAGraph()  # the step as the bench runs it: no host in the loop
 with torch.cuda.graph(graph, stream=stream):
-    for ln, _ in bench.LAUNCHES:
+    for ln, _ in LAUNCHES:
         spmv(Ws[ln], xs[ln], y=ys[ln], stream=stream)
 flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
 for rep in range(3):
@@ -45,7 +46,7 @@ for rep in range(3):
         _lib.check(lib.ecsr_b200_debug_trace(Ws[ln].handle, out.ctypes.data, out.size), "trace")
         tr[ln] = out.reshape(g, 16).astype(np.int64)
     t0 = min(t[:, 0].min() for t in tr.values())
-    np.savez(os.path.join(ROOT, "gpurun_out", f"step_trace_{rep}.npz"), **tr)
+    np.savez(os.path.join(ROOT, "gpurun_out", f"step_trace_q{QPCT}_{rep}.npz"), **tr)
     print(f"rep {rep}: times in us from the step's first CTA start")
     for ln, t in tr.items():
         f = lambda i: (t[:, i] - t0) / 1e3

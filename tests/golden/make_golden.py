@@ -83,6 +83,21 @@ def cases():
         out.append((f"{kind}_{m}x{k}_s{s}_b{bits}_seed{seed}", ref,
                     ExtractionConfig(32, 4, bits),
                     {"kind": kind, "m": m, "k": k, "s": s, "seed": seed}))
+    # edge shapes of SURVEY.md §8(a) a15(6): non-power-of-two warps (lane padding to
+    # lanes_p2, _speedups.pyx:91-93, 120-127; W = 3 is pkg/tests/test_storage.py:99),
+    # v = 2 at W = 32 (generic kernel), a single lane, B = 16 with v = 1
+    for kind, m, k, s, seed, (w, v, bits) in (
+        ("uniform", 96, 120, 0.6, 21, (3, 1, 8)), ("planted", 128, 150, 0.5, 22, (3, 2, 8)),
+        ("uniform", 80, 200, 0.7, 23, (5, 2, 4)), ("planted", 160, 160, 0.6, 24, (6, 4, 8)),
+        ("uniform", 100, 333, 0.8, 25, (7, 1, 16)), ("planted", 256, 256, 0.5, 26, (32, 2, 8)),
+        ("magnitude", 192, 300, 0.6, 27, (32, 1, 16)), ("uniform", 48, 64, 0.5, 28, (1, 1, 8)),
+        ("planted", 200, 256, 0.6, 29, (12, 3, 8)),
+    ):
+        a = make_matrix(kind, m, k, s, seed, dtype=np.float64)
+        ref = core.CsrMatrix(a.num_rows, a.num_cols, a.row_ptr, a.col_idx, a.values)
+        out.append((f"edge_{kind}_{m}x{k}_w{w}v{v}b{bits}_seed{seed}", ref,
+                    ExtractionConfig(w, v, bits),
+                    {"kind": kind, "m": m, "k": k, "s": s, "seed": seed}))
     return out
 
 
@@ -91,9 +106,17 @@ def spmv(ec, x):
 
 
 def main():
+    """`make_golden.py [NAME_PREFIX ...]`: regenerate only the matching cases (the rest
+    of the manifest is kept as is)."""
     _kernels.use_backend("compiled")
+    only = sys.argv[1:]
     manifest = []
+    if only:
+        with open(os.path.join(HERE, "manifest.json")) as fh:
+            manifest = [c for c in json.load(fh) if not any(c["name"].startswith(p) for p in only)]
     for name, mat, cfg, meta in cases():
+        if only and not any(name.startswith(p) for p in only):
+            continue
         ec = storage.convert_csr(mat, cfg, dtype=np.float64)
         blob = storage.serialize(ec)
         x = np.random.default_rng(zlib.crc32(name.encode())).uniform(-1, 1, mat.num_cols)

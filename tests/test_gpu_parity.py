@@ -39,7 +39,8 @@ def test_f16_ordered_bitwise_and_atomic_tolerance(name):
     g = load_golden(name)
     ec, x = g["ec"], g["x"]
     W = to_device(ec)
-    expect_tiled = ec.warp_size == 32 and ec.delta_bits <= 8 and len(ec.sets) > 0
+    expect_tiled = (ec.warp_size == 32 and ec.delta_bits <= 8 and len(ec.sets) > 0
+                    and all(s.vector_size in (1, 4) for s in ec.sets))
     assert (W.layout == "tiled") == expect_tiled
     y_ord = spmv(W, _x16(x), ordered=True).cpu().numpy()
     assert y_ord.dtype == np.float32
@@ -226,68 +227,83 @@ def test_overwrite_mode_zeroes_y_in_kernel_across_graph_replays(name):
             assert rel_err(y.cpu().numpy(), g["y16"]) <= TIGHT_ATOMIC
 
 
-@pytest.mark.parametrize("tile", ["4096", "8192"])
-def test_ring_wraps_many_times_small_tiles(tile, monkeypatch):
+@pytest.mark.parametrize("tile_kb", [4, 8])
+def test_ring_wraps_many_times_small_tiles(tile_kb):
     # records handed out several ring cycles ahead of the producer (regression: parity
-    # aliasing of the full barriers); the tile size is read once per process, so run a
-    # child process with a small ECSR_B200_TILE
-    import subprocess
-    import sys as _sys
-
-    code = (
-        "import numpy as np, torch, oracle;"
-        "from conftest import load_golden;"
-        "from paper_2507_12205_b200.device import spmv, to_device, vstack;"
-        "g = load_golden('planted_512x384_s0.5_b8_seed15');"
-        "ec = vstack([g['ec']] * 6); W = to_device(ec);"
-        "assert W.bytes()['tiles'] > 8 * W.bytes()['stages'];"
-        "x = g['x'];"
-        "y = spmv(W, torch.from_numpy(x.astype(np.float16)).cuda(), ordered=True).cpu().numpy();"
-        "ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),"
-        " x.astype(np.float16).astype(np.float32), np.float32);"
-        "assert np.array_equal(y, ref);"
-        "[spmv(W, torch.from_numpy(x.astype(np.float16)).cuda()) for _ in range(20)];"
-        "torch.cuda.synchronize(); print('ok')"
-    )
-    import os as _os
-    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
-    env = dict(_os.environ, ECSR_B200_TILE=tile,
-               PYTHONPATH=_os.pathsep.join([root, _os.path.join(root, "tests")]))
-    out = subprocess.run([_sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    # aliasing of the full barriers): small tiles (pack flag ECSR_PACK_TILE_KB)
+    g = load_golden("planted_512x384_s0.5_b8_seed15")
+    ec = vstack([g["ec"]] * 6)
+    W = to_device(ec, tile_kb=tile_kb)
+    assert W.bytes()["tiles"] > 8 * W.bytes()["stages"]
+    x = g["x"]
+    y = spmv(W, _x16(x), ordered=True).cpu().numpy()
+    ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),
+                                x.astype(np.float16).astype(np.float32), np.float32)
+    assert np.array_equal(y, ref)
+    ys = [spmv(W, _x16(x)) for _ in range(20)]
+    torch.cuda.synchronize()
+    assert all(rel_err(v.cpu().numpy(), ref) <= TIGHT_ATOMIC for v in ys)
 
 
-@pytest.mark.gpu
 @pytest.mark.parametrize("rows,sparsity,per_cta", [(4096, 0.5, 32), (114688, 0.95, 256)])
 def test_many_tiles_per_cta_wrap_stage_map(rows, sparsity, per_cta):
     # > 32 tiles per CTA: the producer's 32-tile record-count window slides and the
-    # 32-entry tile -> stage map wraps many times (tiny tiles, one record each); > 256:
+    # 32-entry tile -> stage map wraps many times (1 KB tiles, one record each); > 256:
     # the consumers' shared prefix-count cache overflows to global loads
-    import subprocess
-    import sys as _sys
+    from paper_2507_12205_b200.encoder import convert_csr
+    from paper_2507_12205_b200.generators import make_matrix
 
-    code = (
-        "import numpy as np, torch, oracle;"
-        "from paper_2507_12205_b200.device import spmv, to_device;"
-        "from paper_2507_12205_b200.encoder import convert_csr;"
-        "from paper_2507_12205_b200.generators import make_matrix;"
-        f"ec = convert_csr(make_matrix('magnitude', {rows}, 4096, {sparsity}, 7, dtype=np.float32));"
-        "W = to_device(ec); b = W.bytes();"
-        f"assert b['tiles'] > {per_cta} * b['grid'], (b['tiles'], b['grid']);"
-        "x = np.random.default_rng(2).uniform(-1, 1, 4096);"
-        "xd = torch.from_numpy(x.astype(np.float16)).cuda();"
-        "ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),"
-        " x.astype(np.float16).astype(np.float32), np.float32);"
-        "y = spmv(W, xd, ordered=True).cpu().numpy(); assert np.array_equal(y, ref);"
-        "ys = [spmv(W, xd).cpu().numpy() for _ in range(5)];"
-        "assert all(np.max(np.abs(v - ref)) <= 1e-5 * np.max(np.abs(ref)) for v in ys);"
-        "print('ok')"
-    )
-    import os as _os
-    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
-    env = dict(_os.environ, ECSR_B200_TILE="1024",
-               PYTHONPATH=_os.pathsep.join([root, _os.path.join(root, "tests")]))
-    out = subprocess.run([_sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    ec = convert_csr(make_matrix("magnitude", rows, 4096, sparsity, 7, dtype=np.float32))
+    W = to_device(ec, tile_kb=1)
+    b = W.bytes()
+    assert b["tiles"] > per_cta * b["grid"], (b["tiles"], b["grid"])
+    x = np.random.default_rng(2).uniform(-1, 1, 4096)
+    xd = _x16(x)
+    ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),
+                                x.astype(np.float16).astype(np.float32), np.float32)
+    y = spmv(W, xd, ordered=True).cpu().numpy()
+    assert np.array_equal(y, ref)
+    for _ in range(5):
+        assert rel_err(spmv(W, xd).cpu().numpy(), ref) <= TIGHT_ATOMIC
+
+
+def test_concurrent_streams_share_one_handle():
+    # one handle, two streams, launches interleaved without host syncs: each stream has
+    # its own workspace (gate counter, partials), so overwrite mode (grid gate) and
+    # ordered mode (partials) stay exact while the launches overlap
+    g = load_golden("planted_512x384_s0.5_b8_seed15")
+    ec = vstack([g["ec"]] * 8)
+    W = to_device(ec)
+    rng = np.random.default_rng(11)
+    xs = [rng.uniform(-1, 1, ec.num_cols) for _ in range(2)]
+    refs = [oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),
+                                  x.astype(np.float16).astype(np.float32), np.float32) for x in xs]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    xd = [_x16(x) for x in xs]
+    ys = [[torch.empty(ec.num_rows, device="cuda") for _ in range(16)] for _ in range(2)]
+    torch.cuda.synchronize()
+    for i in range(16):
+        for s in range(2):
+            spmv(W, xd[s], y=ys[s][i], ordered=(i % 4 == 3), stream=streams[s])
+    torch.cuda.synchronize()
+    for s in range(2):
+        for i, y in enumerate(ys[s]):
+            got = y.cpu().numpy()
+            if i % 4 == 3:
+                assert np.array_equal(got, refs[s])
+            else:
+                assert rel_err(got, refs[s]) <= TIGHT_ATOMIC
+
+
+def test_fifth_stream_is_rejected_and_device_checked():
+    g = load_golden("planted_512x384_s0.5_b8_seed15")
+    W = to_device(g["ec"])
+    x = _x16(g["x"])
+    streams = [torch.cuda.Stream() for _ in range(5)]
+    for s in streams[:4]:
+        spmv(W, x, stream=s)
+    with pytest.raises(ValueError, match="other streams"):
+        spmv(W, x, stream=streams[4])
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError):
+        spmv(W, x, y=torch.empty(W.num_rows))  # host y
