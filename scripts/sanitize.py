@@ -1,0 +1,66 @@
+"""Workload for compute-sanitizer (racecheck / synccheck / memcheck / initcheck) of the
+tiled kernel: small containers, every launch mode, checked against the oracle.
+
+    compute-sanitizer --tool racecheck python scripts/sanitize.py
+
+Covers: the smoke container (one tile per CTA), a 1024x4096 matrix packed with 1 KB
+tiles (many tiles per CTA: the stage pool, the tile->stage map and the tail queue
+wrap), the u32-base (K > 65535) variant, two streams sharing one handle, and
+overwrite / accumulate / ordered modes."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_2507_12205_b200.container import deserialize  # noqa: E402
+from paper_2507_12205_b200.device import spmv, to_device  # noqa: E402
+from paper_2507_12205_b200.encoder import convert_csr  # noqa: E402
+from paper_2507_12205_b200.generators import make_matrix  # noqa: E402
+
+
+def ref16(ec, x):
+    return oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32),
+                                 x.astype(np.float16).astype(np.float32), np.float32)
+
+
+def check(ec, W, x, label):
+    xd = torch.from_numpy(x.astype(np.float16)).cuda()
+    r = ref16(ec, x)
+    y = spmv(W, xd, ordered=True).cpu().numpy()
+    assert np.array_equal(y, r), label + ": ordered"
+    yf = torch.empty(W.num_rows, device="cuda")
+    for _ in range(3):
+        spmv(W, xd, y=yf)
+    e = np.max(np.abs(yf.cpu().numpy() - r)) / max(np.max(np.abs(r)), 1e-30)
+    assert e <= 1e-5, (label, e)
+    spmv(W, xd, y=yf, accumulate=True)
+    e = np.max(np.abs(yf.cpu().numpy() - 2 * r)) / max(np.max(np.abs(r)), 1e-30)
+    assert e <= 1e-5, (label, "accumulate", e)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ya, yb = torch.empty_like(yf), torch.empty_like(yf)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        spmv(W, xd, y=ya, stream=s1)
+        spmv(W, xd, y=yb, stream=s2)
+    torch.cuda.synchronize()
+    for v in (ya, yb):
+        e = np.max(np.abs(v.cpu().numpy() - r)) / max(np.max(np.abs(r)), 1e-30)
+        assert e <= 1e-5, (label, "two streams", e)
+    print(f"{label}: ok", flush=True)
+
+
+z = np.load(os.path.join(ROOT, "tests", "golden", "planted_512x384_s0.5_b8_seed15.npz"))
+ec = deserialize(z["blob"].tobytes())
+check(ec, to_device(ec), z["x"], "smoke 512x384")
+ec = convert_csr(make_matrix("magnitude", 1024, 4096, 0.5, 7, dtype=np.float32))
+W = to_device(ec, tile_kb=1)
+print("tiles", W.bytes()["tiles"], "grid", W.bytes()["grid"], "queue", W.bytes()["queue_tiles"])
+check(ec, W, np.random.default_rng(1).uniform(-1, 1, 4096), "1024x4096 1 KB tiles")
+ec = convert_csr(make_matrix("magnitude", 256, 70000, 0.995, 9, dtype=np.float32))
+check(ec, to_device(ec), np.random.default_rng(2).uniform(-1, 1, 70000), "256x70000 wide bases")
+print("sanitize workload done")
