@@ -5,8 +5,10 @@ Headline workload ("llama7b-layer-s0.5", configs[1]): the seven SpMVs of one LLa
 decoder layer at 50 % per-row magnitude pruning (random N(0, 1/K) weights, seeded),
 EC-CSR-encoded with W=32, V=4, B=8 (`storage.convert_csr`, storage.py:700-708):
 q, k, v, o 4096x4096, gate, up 11008x4096, down 4096x11008. One step = the layer's
-SpMVs as 4 stream-ordered launches (q|k|v and gate|up row-stacked, because they share
-x; o; down), each y = W x with fp16 values and x, fp32 accumulate and y.
+SpMVs, y = W x with fp16 values and x, fp32 accumulate and y, as 4 matrix sets (q|k|v
+and gate|up row-stacked, because they share x; o; down) whose inputs are all ready at
+the step's start, so they run as ONE grouped launch (ecsr_b200_group_spmv). The same
+step as 4 PDL-chained launches is reported beside it ("chained").
 
 Encodings: every container is sha256-checked against the REFERENCE encoder's output
 (tests/golden/ref_hashes.json, made by scripts/ref_hashes.py with the reference's own
@@ -437,16 +439,18 @@ def load_workload(name=HEADLINE):
     return ecs, {"source": src, "sha256_matches_pinned": ok}
 
 
-def check_parity(name, ecs, handles, xs, ys, stream):
+def check_parity(name, ecs, handles, xs, ys, stream, group=None):
     """Every launch of the workload against the oracle (the reference kernel's
     arithmetic, oracle/liboracle.so): ordered mode bitwise on fp16-rounded inputs, fast
-    mode rel-inf <= 1e-5 of that and rel-L2 <= 1e-3 of the FP32 result (north_star)."""
+    mode rel-inf <= 1e-5 of that and rel-L2 <= 1e-3 of the FP32 result (north_star) --
+    each matrix set launched alone, and all of them in the step's grouped launch."""
     import torch
 
     import oracle
     from paper_2507_12205_b200.device import spmv
 
     out = {}
+    refs = {}
     for ln, names in WORKLOADS[name]["launches"]:
         x16 = xs[ln].cpu().numpy()
         x32 = x16.astype(np.float32)
@@ -465,8 +469,23 @@ def check_parity(name, ecs, handles, xs, ys, stream):
         rel_l2 = float(np.linalg.norm(y_fast.astype(np.float64) - y32) / max(np.linalg.norm(y32), 1e-30))
         bitwise = bool(np.array_equal(y_ord, y16))
         out[ln] = {"ordered_bitwise": bitwise, "fast_rel_inf": rel_inf, "fast_rel_l2_vs_fp32": rel_l2}
+        refs[ln] = (y16, y32)
         if not bitwise or rel_inf > 1e-5 or rel_l2 > 1e-3:
             raise SystemExit(f"parity guard failed on {name}/{ln}: {out[ln]}")
+    if group is not None:
+        lns = [ln for ln, _ in WORKLOADS[name]["launches"]]
+        for y in ys.values():
+            y.fill_(float("nan"))
+        group.spmv([xs[ln] for ln in lns], [ys[ln] for ln in lns], stream=stream)
+        torch.cuda.synchronize()
+        for ln in lns:
+            y16, y32 = refs[ln]
+            got = ys[ln].cpu().numpy().astype(np.float64)
+            rel_inf = float(np.max(np.abs(got - y16))) / max(float(np.max(np.abs(y16))), 1e-30)
+            rel_l2 = float(np.linalg.norm(got - y32) / max(np.linalg.norm(y32), 1e-30))
+            out[ln].update({"grouped_rel_inf": rel_inf, "grouped_rel_l2_vs_fp32": rel_l2})
+            if not rel_inf <= 1e-5 or not rel_l2 <= 1e-3:
+                raise SystemExit(f"parity guard failed on {name}/{ln} (grouped launch): {out[ln]}")
     return out
 
 
@@ -488,6 +507,10 @@ class Workload:
         self.launch_bytes = {ln: sum(self.mbytes[n] for n in names) for ln, names in self.launches}
         self.handles = {ln: to_device(vstack([self.ecs[n] for n in names]), device=dev)
                         for ln, names in self.launches}
+        # the step's launches have independent inputs: one grouped launch runs them all
+        from paper_2507_12205_b200.device import SpmvGroup
+
+        self.group = SpmvGroup([self.handles[ln] for ln, _ in self.launches])
         xs16 = launch_inputs(name)
 
         def pad8(n):
@@ -510,24 +533,32 @@ class Workload:
             self.xs[ln] = self.x_all[xo:xo + len(xs16[ln])]
             self.ys[ln] = self.y_all[yo:yo + self.handles[ln].num_rows]
             xo, yo = xo + k, yo + mm
+        self.x_list = [self.xs[ln] for ln, _ in self.launches]
+        self.y_list = [self.ys[ln] for ln, _ in self.launches]
 
     def step(self, stream):
+        """One step: the layer's products in ONE grouped launch."""
+        self.group.spmv(self.x_list, self.y_list, stream=stream)
+
+    def step_chained(self, stream):
+        """The same step as one launch per matrix set (stream-ordered, PDL-chained)."""
         from paper_2507_12205_b200.device import spmv
 
         for ln, _ in self.launches:
             spmv(self.handles[ln], self.xs[ln], y=self.ys[ln], stream=stream)
 
-    def graph(self, stream, steps):
+    def graph(self, stream, steps, chained=False):
         import torch
 
+        body = self.step_chained if chained else self.step
         with torch.cuda.stream(stream):
             for _ in range(2):
-                self.step(stream)
+                body(stream)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for _ in range(steps):
-                self.step(stream)
+                body(stream)
         return g
 
 
@@ -572,7 +603,7 @@ def bench_extra(name, dev, stream, args, peak):
     t0 = time.perf_counter()
     wl = Workload(name, dev)
     setup_s = time.perf_counter() - t0
-    par = check_parity(name, wl.ecs, wl.handles, wl.xs, wl.ys, stream)
+    par = check_parity(name, wl.ecs, wl.handles, wl.xs, wl.ys, stream, group=wl.group)
     out = {"workload": name, "desc": WORKLOADS[name]["desc"],
            "config": workload_config(name, wl.step_bytes), "parity": par,
            "inputs": wl.inputs, "setup_s": round(setup_s, 1)}
@@ -581,9 +612,14 @@ def bench_extra(name, dev, stream, args, peak):
         g = wl.graph(stream, spg)
         ms, _ = time_graph(g, max(2, args.steps // spg), 2, stream)
         ms /= spg
+        gc = wl.graph(stream, spg, chained=True)
+        ms_c, _ = time_graph(gc, max(2, args.steps // spg), 2, stream)
+        ms_c /= spg
         gbs = wl.step_bytes / (ms * 1e-3) / 1e9
         out.update({"value": round(gbs, 1), "unit": "GB/s", "ms_per_step": round(ms, 5),
-                    "frac": round(gbs / peak, 4), "steps_per_graph": spg})
+                    "frac": round(gbs / peak, 4), "steps_per_graph": spg, "launches_per_step": 1,
+                    "chained": {"value": round(wl.step_bytes / (ms_c * 1e-3) / 1e9, 1),
+                                "ms_per_step": round(ms_c, 5), "launches_per_step": len(wl.launches)}})
     else:
         g = wl.graph(stream, 1)
         flush = torch.empty(128 << 20, dtype=torch.float32, device=dev)
@@ -646,13 +682,13 @@ def run_ours(args):
 
     wl = Workload(HEADLINE, dev)
     stream = torch.cuda.Stream(dev)
-    parity = check_parity(HEADLINE, wl.ecs, wl.handles, wl.xs, wl.ys, stream)
+    parity = check_parity(HEADLINE, wl.ecs, wl.handles, wl.xs, wl.ys, stream, group=wl.group)
 
     # device-resident timing: a CUDA graph of `spg` consecutive steps (layers), replayed
     # steps/spg times -- a decode graph holds a model's consecutive layers, so launches
     # chain through PDL across layers as they do in deployment; exactly K steps are timed
     spg = max(d for d in range(1, 9) if args.steps % d == 0)
-    graph = wl.graph(stream, spg)
+    graph = wl.graph(stream, spg)  # one grouped launch per step
     with torch.cuda.stream(stream):
         for _ in range(max(1, args.warmup // spg)):
             graph.replay()
@@ -666,6 +702,10 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    # the same steps as one launch per matrix set (PDL-chained), for comparison
+    graph_c = wl.graph(stream, spg, chained=True)
+    ms_chained, _ = time_graph(graph_c, args.steps // spg, max(1, args.warmup // spg), stream)
+    ms_chained /= spg
 
     # per-launch device time of each launch kind: a graph of that launch alone, replayed
     # after the whole layer (284 MB > L2) streamed through, CUDA events around it
@@ -692,43 +732,18 @@ def run_ours(args):
                 tot += a.elapsed_time(b)
         launch_ms[ln] = tot / n
 
-    # end-to-end through the public API: pinned host x in, y out, every step. The first
-    # launch's x and the last launch's y are on the critical path; the other inputs go
-    # up, and the other outputs come back, on a side stream while launches run.
+    # end-to-end through the public API: pinned host x in, y out, every step (one H2D
+    # of every x, the grouped launch, one D2H of every y)
     h2d = sum(x.numel() * 2 for x in wl.xs_host.values())
     d2h = sum(y.numel() * 4 for y in wl.ys_host.values())
-    side = torch.cuda.Stream(dev)
-    first, last = wl.launches[0][0], wl.launches[-1][0]
-    k0 = wl.xs[first].numel()
-    y_last0 = wl.ys[last].data_ptr() - wl.y_all.data_ptr()
-    y_last0 //= 4
 
     def e2e_body():
-        fork = torch.cuda.Event()
-        fork.record(stream)
-        side.wait_event(fork)
-        wl.x_all[:k0].copy_(wl.x_host_all[:k0], non_blocking=True)
-        with torch.cuda.stream(side):
-            wl.x_all[k0:].copy_(wl.x_host_all[k0:], non_blocking=True)
-            x_rest = torch.cuda.Event()
-            x_rest.record(side)
-        head_done = torch.cuda.Event()
-        for i, (ln, _) in enumerate(wl.launches):
-            if i == 1:
-                stream.wait_event(x_rest)
-            spmv(wl.handles[ln], wl.xs[ln], y=wl.ys[ln], stream=stream)
-            if i == len(wl.launches) - 2:
-                head_done.record(stream)
-        with torch.cuda.stream(side):
-            side.wait_event(head_done)
-            wl.y_host_all[:y_last0].copy_(wl.y_all[:y_last0], non_blocking=True)
-            y_head = torch.cuda.Event()
-            y_head.record(side)
-        wl.y_host_all[y_last0:].copy_(wl.y_all[y_last0:], non_blocking=True)
-        stream.wait_event(y_head)  # join
+        wl.x_all.copy_(wl.x_host_all, non_blocking=True)
+        wl.step(stream)
+        wl.y_host_all.copy_(wl.y_all, non_blocking=True)
 
     # the same step with its host<->device copies, captured once (pinned-host memcpy
-    # nodes + the 4 launches) so host API overhead does not dominate ~70 us steps
+    # nodes + the launch) so host API overhead does not dominate ~60 us steps
     g_e2e = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_e2e, stream=stream):
         e2e_body()
@@ -746,7 +761,7 @@ def run_ours(args):
         with open(prof) as fh:
             per_step = json.load(fh).get("dram_bytes_per_step")
         if per_step:
-            traffic = round(per_step / len(wl.launches))
+            traffic = round(per_step)  # one grouped launch per step
     layout = {ln: W.bytes() for ln, W in wl.handles.items()}
     line = {
         "metric": METRIC,
@@ -755,23 +770,26 @@ def run_ours(args):
         "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16 values/x, f32 accumulate", "data": "synthetic",
         "config": workload_config(HEADLINE, wl.step_bytes),
-        "steps_per_graph": spg, "parallelism": "single",
+        "steps_per_graph": spg, "parallelism": "single", "launches_per_step": 1,
+        "chained": {"value": round(wl.step_bytes / (ms_chained * 1e-3) / 1e9, 1), "unit": "GB/s",
+                    "ms_per_step": round(ms_chained, 5), "launches_per_step": len(wl.launches),
+                    "note": "the same step as one launch per matrix set, PDL-chained"},
         "latency_us": {ln: round(v * 1e3, 2) for ln, v in launch_ms.items()},
         "e2e": {"value": round(wl.step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_launch": round(wl.step_bytes / len(wl.launches)),
+                     "algorithmic_bytes_per_launch": wl.step_bytes,
                      "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel",
                      "device_arena_bytes": {ln: layout[ln]["device_arena_bytes"] for ln in layout}},
         "parity": parity,
         "inputs": wl.inputs,
-        "gpu_launches": len(wl.launches) * args.steps,
+        "gpu_launches": args.steps,
         "clocks": clocks.summary(),
     }
     mbytes = dict(wl.mbytes)
-    del wl, graph, g_e2e
+    del wl, graph, graph_c, g_e2e
     torch.cuda.synchronize()
     if not args.no_extra:
         line["configs"] = [bench_extra(n, dev, stream, args, peak)
@@ -822,7 +840,7 @@ def run_sharded(args):
     import torch.distributed as dist
 
     from paper_2507_12205_b200 import to_device
-    from paper_2507_12205_b200.device import spmv, vstack
+    from paper_2507_12205_b200.device import vstack
     from paper_2507_12205_b200.sharded import ShardPlan
 
     rank, local_rank, world = dist_env()
@@ -872,9 +890,14 @@ def run_sharded(args):
     yfull_host = {ln: torch.empty(yfull[ln].shape, dtype=torch.float32).pin_memory() for ln in yfull}
     stream = torch.cuda.Stream(dev)
 
-    def spmvs():
-        for ln, _ in launches:
-            spmv(handles[ln], xs[ln], y=send[offs[ln]:offs[ln] + handles[ln].num_rows], stream=stream)
+    from paper_2507_12205_b200.device import SpmvGroup
+
+    group = SpmvGroup([handles[ln] for ln, _ in launches])
+    x_list = [xs[ln] for ln, _ in launches]
+    y_list = [send[offs[ln]:offs[ln] + handles[ln].num_rows] for ln, _ in launches]
+
+    def spmvs():  # this rank's shard of every matrix set: one grouped launch
+        group.spmv(x_list, y_list, stream=stream)
 
     def exchange():
         dist.all_gather_into_tensor(recv, send)
@@ -969,7 +992,7 @@ def run_sharded(args):
                          "peak": peak, "unit": "GB/s per GPU",
                          "frac": round(step_bytes / world / (ms * 1e-3) / 1e9 / peak, 4),
                          "traffic": None, "peak_source": peak_kind, "kernel": "ecsr_tiled_kernel"},
-            "gpu_launches": len(launches) * args.steps,
+            "gpu_launches": args.steps,
             "clocks": clocks.summary(),
             "sharded": {"spmv_ms_per_step": round(spmv_ms, 5), "exchange_ms_per_step": round(gather_ms, 5),
                         "step_ms": round(ms, 5), "allgather_bytes_per_rank_per_step": int(send.numel()) * 4,

@@ -62,6 +62,10 @@ extern "C" {
 #define ECSR_SPMV_ORDERED 2     /* OR-flag: per-block partials + ordered per-row sum;
                                    bitwise-reproducible, reference order
                                    (executor.py:89 + _speedups.pyx:128-129) */
+#define ECSR_SPMV_MEMSET_Y 4    /* OR-flag: overwrite through a memset of y and a launch
+                                   without the in-kernel zero-y gate (the path taken
+                                   automatically when the whole grid cannot be resident:
+                                   green-context SM partitions, MPS thread percentage) */
 
 /* One block set, exactly the arrays of ecsr.storage.EcCsrSet (storage.py:50-62). */
 typedef struct ecsr_host_set {
@@ -130,6 +134,23 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
  * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream). */
 int ecsr_b200_spmv(const ecsr_dev* dev, const void* x, void* y, int32_t mode, void* stream);
 
+/* Grouped launch: k <= 8 independent products y_i = A_i x_i in one launch of the tiled
+ * kernel -- two when the members mix x sizes on both sides of 32 KB (one launch per
+ * CTAs-per-SM class). Every member must use the tiled layout, on one device, all with
+ * K <= 65535 or all above. The members' CTAs run side by side, so the group pays one
+ * launch ramp and one tail instead of k (e.g. the projections of a decoder layer whose
+ * inputs are all ready). The handles must outlive the group. xs / ys: host arrays of k
+ * device pointers, read at call time (graph capture records them). Modes as
+ * ecsr_b200_spmv; ORDERED runs the members one after another (bitwise reproducible).
+ * Like a handle, a group keeps one launch workspace per stream (up to 4 streams).
+ * ecsr_b200_group_info: launches per call, total CTAs, CTAs per member (ctas[k]). */
+typedef struct ecsr_group ecsr_group;
+int ecsr_b200_group_create(const ecsr_dev* const* mats, int32_t k, ecsr_group** out);
+int ecsr_b200_group_spmv(const ecsr_group* group, const void* const* xs, void* const* ys,
+                         int32_t mode, void* stream);
+int ecsr_b200_group_info(const ecsr_group* group, int32_t* launches, int32_t* grid, int32_t* ctas,
+                         int32_t k);
+void ecsr_b200_group_free(ecsr_group* group);
 /* .ecsr wire format (storage.py:389-483) straight to a device handle, no numpy round trip
  * (SURVEY.md §8(f) #3). ecsr_b200_parse parses and shape-checks a blob on the host only,
  * rejecting corruption with the reference's ContainerError (code 1) and message: bad
@@ -162,6 +183,26 @@ int ecsr_b200_unpack(const ecsr_dev* dev, ecsr_out_set* out, int32_t nsets,
 int ecsr_b200_bytes(const ecsr_dev* dev, ecsr_bytes* out);
 void ecsr_b200_free(ecsr_dev* dev);
 
+/* Access trace of the device layout (the reference's
+ * spmv_ec_traced + check_coalescing, executor.py:106-221): one entry per block, warp
+ * step and array (0 = deltas, 1 = values) in the order the kernel reads them, mapped
+ * back to the reference span it carries (`warp` = the block's index in container order,
+ * `start`/`span` in elements of the set's delta_indices / block_values) and located in
+ * device memory (`dev_offset`/`dev_bytes`: bytes into the tiled arena, or into the
+ * generic layout's u32 delta / value arrays; `lane_bytes`: width of each lane's load).
+ * Writes min(cap, count) entries; `count` gets the total (call with cap 0 to size). */
+typedef struct ecsr_trace_rec {
+    int64_t warp;
+    int32_t step;
+    int32_t array;
+    int32_t set_index;
+    int32_t lane_bytes;
+    int64_t start;
+    int64_t span;
+    int64_t dev_offset;
+    int64_t dev_bytes;
+} ecsr_trace_rec;
+int ecsr_b200_trace(const ecsr_dev* dev, ecsr_trace_rec* out, int64_t cap, int64_t* count);
 /* The reference backend protocol entry (_speedups.pyx:55-78): host arrays, one set,
  * y (host, y_dtype ECSR_F32 or ECSR_F64) accumulated in place in the canonical
  * order. values/x are given in y's precision (the shim coerces like

@@ -6,6 +6,7 @@ Public API (names follow the reference `ecsr` package, pkg/src/ecsr/__init__.py)
     load_device(path | bytes)              .ecsr blob -> DeviceMatrix in one native call
     parse_blob(path | bytes)               native host-only parse + shape check of a blob
     spmv(W, x) -> y                        y = W x on the GPU (fp16 in, fp32 accumulate)
+    group([W1, W2, ..]).spmv([x1, x2, ..]) independent products in ONE launch
     spmv_ec(ec, x)                         executor.spmv_ec-compatible convenience
     EcCsrMatrix / EcCsrSet, serialize, deserialize, storage_components,
     kernel_model_bytes, validate_container  host container (storage.py mirror)
@@ -54,6 +55,13 @@ def spmv(W, x, y=None, accumulate: bool = False, ordered: bool = False, stream=N
     from .device import spmv as _spmv
 
     return _spmv(W, x, y=y, accumulate=accumulate, ordered=ordered, stream=stream)
+
+
+def group(mats):
+    """One launch for several independent products (device.SpmvGroup)."""
+    from .device import SpmvGroup
+
+    return SpmvGroup(mats)
 
 
 def spmv_ec(ec, x, ordered: bool = True):

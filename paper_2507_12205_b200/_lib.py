@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 OK, ERR_CONTAINER, ERR_VALUE, ERR_CUDA = 0, 1, 2, 3
 F16, F32, F64 = 1, 2, 3
 PACK_DEFAULT, PACK_FORCE_GENERIC = 0, 1
-SPMV_OVERWRITE, SPMV_ACCUMULATE, SPMV_ORDERED = 0, 1, 2
+SPMV_OVERWRITE, SPMV_ACCUMULATE, SPMV_ORDERED, SPMV_MEMSET_Y = 0, 1, 2, 4
 
 _DTYPE_CODE = {np.dtype(np.float16): F16, np.dtype(np.float32): F32, np.dtype(np.float64): F64}
 
@@ -80,6 +80,12 @@ SIGNATURES = {
     "ecsr_b200_unpack": (c_i32, [c_vp, ctypes.POINTER(OutSet), c_i32, c_i32]),
     "ecsr_b200_bytes": (c_i32, [c_vp, ctypes.POINTER(Bytes)]),
     "ecsr_b200_free": (None, [c_vp]),
+    "ecsr_b200_group_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, ctypes.POINTER(c_vp)]),
+    "ecsr_b200_group_spmv": (c_i32, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i32, c_vp]),
+    "ecsr_b200_group_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
+                                     ctypes.POINTER(c_i32), c_i32]),
+    "ecsr_b200_group_free": (None, [c_vp]),
+    "ecsr_b200_trace": (c_i32, [c_vp, c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "ecsr_b200_spmv_set": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_i64, c_i32]),
     "ecsr_b200_to_f16": (c_i32, [c_vp, c_i32, c_vp, c_i64]),

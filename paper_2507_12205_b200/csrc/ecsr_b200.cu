@@ -7,6 +7,7 @@
 //   * build the slot tables of the ordered (bitwise-reproducible) y reduction;
 //   * keep the cold section (pad_mask, set descriptors) on the host for exact unpack;
 //   * expose the reference backend-protocol call spmv_set (_speedups.pyx:55-78).
+#include <cuda.h>  // driver API types only (entry points via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -56,7 +57,11 @@ int tile_target() {
 int pre_tiles() { return std::max(1, env_int("ECSR_B200_PRE", 2)); }
 bool trace_enabled() { return env_int("ECSR_B200_TRACE", 0) != 0; }
 bool trace_caller_resets() { return env_int("ECSR_B200_TRACE", 0) == 2; }
+bool coop_launch() { return env_int("ECSR_B200_COOP", 0) != 0; }
+bool group_force_cps1() { return env_int("ECSR_B200_GROUP_CPS1", 0) != 0; }
 #else
+constexpr bool coop_launch() { return false; }
+constexpr bool group_force_cps1() { return false; }
 int tile_target() { return t_tile_override ? t_tile_override : g_tile_default; }
 int pre_tiles() { return 2; }  // tiles streamed before griddepcontrol.wait and the x copy
 constexpr bool trace_enabled() { return false; }
@@ -196,10 +201,12 @@ struct ecsr_dev {
     int64_t arena_bytes = 0;
     uint32_t* d_tile_start16 = nullptr;
     int64_t ntiles = 0;
-    uint32_t* d_cta_tile = nullptr;        // [2 * grid] static tile range of each CTA
+    uint4* d_cta_work = nullptr;           // [grid] {member 0, tile lo, tile hi, slice} of each CTA
+    double total_cost = 0;                 // summed tile cost (group CTA split)
     uint32_t* d_tile_meta = nullptr;       // [2 * ntiles] {start16, nrec | bytes16 << 16}
     uint32_t queue_begin = 0, nqueue = 0;  // the launch's tail-queue tiles
     bool lean = false;                     // every run uses a lean-kernel record variant
+    bool gate_ok = true;                   // the whole grid can be resident (zero-y gate)
     int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
     std::vector<TileFeat> tile_feat;       // per tile (cost-model calibration)
     std::vector<uint32_t> cta_tile_h;      // host copy of the CTA tile boundaries
@@ -214,7 +221,7 @@ struct ecsr_dev {
     // concurrently. Allocated at pack time: nothing is allocated on the launch path
     // (safe under CUDA graph capture).
     struct Workspace {
-        unsigned long long* sync = nullptr;  // zero-y grid-gate generation counter (own 128-B line)
+        unsigned long long* gate = nullptr;  // zero-y gate words (ecsr_kernels.cuh: kGate*)
         uint32_t* queue = nullptr;           // tail queue {next tile, CTAs done} (own 128-B line)
         void* partials = nullptr;            // [nslots] ordered-mode block partials
     };
@@ -323,6 +330,40 @@ struct DeviceLimits {
     int smem_optin = 232448;
     int smem_per_sm = 233472;
 };
+
+// SMs the current context may keep busy at once: the device's, reduced to a green
+// context's SM partition (cuCtxGetDevResource) and to the MPS active-thread percentage
+// (CUDA_MPS_ACTIVE_THREAD_PERCENTAGE). The zero-y gate needs the whole grid resident.
+int usable_sms(int device_sms) {
+    using GetCurrent = CUresult (*)(CUcontext*);
+    using GetResource = CUresult (*)(CUcontext, CUdevResource*, CUdevResourceType);
+    static GetCurrent get_current = nullptr;
+    static GetResource get_resource = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_current = reinterpret_cast<GetCurrent>(f);
+        if (cudaGetDriverEntryPoint("cuCtxGetDevResource", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_resource = reinterpret_cast<GetResource>(f);
+        cudaGetLastError();
+    });
+    int sms = device_sms;
+    CUcontext ctx = nullptr;
+    if (get_current && get_resource && get_current(&ctx) == CUDA_SUCCESS && ctx) {
+        CUdevResource r{};
+        if (get_resource(ctx, &r, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS && r.sm.smCount > 0)
+            sms = std::min<int>(sms, static_cast<int>(r.sm.smCount));
+    }
+    if (const char* e = std::getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE")) {
+        const double pct = std::atof(e);
+        if (pct > 0 && pct < 100) sms = std::min(sms, std::max(1, static_cast<int>(sms * pct / 100.0)));
+    }
+    return sms;
+}
 
 int query_limits(int device, DeviceLimits* lim) {
     ECSR_CUDA(cudaDeviceGetAttribute(&lim->sms, cudaDevAttrMultiProcessorCount, device));
@@ -575,6 +616,9 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
     tile_start16->push_back(static_cast<uint32_t>(arena->size() / 16));
 }
 
+// Zero-y gate words of a launch (one counter on its own 128-B line).
+size_t gate_bytes(int) { return 8 * ecsr::kGateWords; }
+
 int build_slots(ecsr_dev* d, const ecsr_host_set* sets, int nsets, int64_t* total) {
     std::vector<uint32_t> cnt(d->M + 1, 0);
     for (int si = 0; si < nsets; ++si) {
@@ -609,16 +653,17 @@ int build_slots(ecsr_dev* d, const ecsr_host_set* sets, int nsets, int64_t* tota
     uint8_t* part = nullptr;
     ECSR_CUDA(cudaMalloc(&part, pbytes * ecsr_dev::kStreamSlots));
     d->allocs.push_back(part);
-    unsigned long long* sync = nullptr;  // two 128-B lines per workspace: gate, queue
-    ECSR_CUDA(cudaMalloc(&sync, 256 * ecsr_dev::kStreamSlots));
+    const size_t wbytes = gate_bytes(d->grid) + 128;  // gate words, then the queue's own line
+    uint8_t* sync = nullptr;
+    ECSR_CUDA(cudaMalloc(&sync, wbytes * ecsr_dev::kStreamSlots));
     d->allocs.push_back(sync);
-    ECSR_CUDA(cudaMemset(sync, 0, 256 * ecsr_dev::kStreamSlots));
+    ECSR_CUDA(cudaMemset(sync, 0, wbytes * ecsr_dev::kStreamSlots));
     for (int i = 0; i < ecsr_dev::kStreamSlots; ++i) {
         d->ws[i].partials = part + pbytes * i;
-        d->ws[i].sync = sync + 32 * i;
-        d->ws[i].queue = reinterpret_cast<uint32_t*>(sync + 32 * i + 16);
+        d->ws[i].gate = reinterpret_cast<unsigned long long*>(sync + wbytes * i);
+        d->ws[i].queue = reinterpret_cast<uint32_t*>(sync + wbytes * i + gate_bytes(d->grid));
     }
-    *total += static_cast<int64_t>(pbytes * ecsr_dev::kStreamSlots + 256 * ecsr_dev::kStreamSlots);
+    *total += static_cast<int64_t>((pbytes + wbytes) * ecsr_dev::kStreamSlots);
     return ECSR_OK;
 }
 
@@ -730,19 +775,78 @@ struct DeviceGuard {
 };
 
 template <typename K, typename... Args>
-cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                       Args... args) {
+cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, bool coop,
+                      Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <typename K, typename... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+    return launch_ex(kernel, grid, block, smem, stream, false, args...);
+}
+
+// One launch of the tiled kernel over `n` members (a single handle, or a group).
+struct MemberLaunch {
+    const ecsr_dev* d;
+    const void* x;
+    void* y;
+    uint32_t* queue;   // the member's tail-queue words in the launch's workspace
+    void* partials;    // ordered mode
+    int ctas;          // CTAs of the launch working on this member
+    int nstages;       // stage-pool depth of its CTAs (the handle's, or a group's)
+};
+
+cudaError_t launch_tiled(const MemberLaunch* m, int n, const uint4* cta_work, int grid, int nc, bool lean,
+                         int smem, unsigned long long* gate, bool ordered, bool zero_y,
+                         unsigned long long* trace, cudaStream_t st) {
+    ecsr::TiledParams p{};
+    int pre = pre_tiles();
+    for (int i = 0; i < n; ++i) {
+        const ecsr_dev* d = m[i].d;
+        ecsr::TiledMember& t = p.mem[i];
+        t.arena = d->d_arena;
+        t.tile_meta = reinterpret_cast<const uint2*>(d->d_tile_meta);
+        t.x = static_cast<const __half*>(m[i].x);
+        t.y = static_cast<float*>(m[i].y);
+        t.partials = static_cast<float*>(m[i].partials);
+        t.queue = m[i].queue;
+        t.M = d->M;
+        t.queue_begin = d->queue_begin;
+        t.nqueue = d->nqueue;
+        t.K = static_cast<int32_t>(d->K);
+        t.stage_bytes = d->stage_bytes;
+        t.nstages = m[i].nstages;
+        t.x_vec16 = (reinterpret_cast<uintptr_t>(m[i].x) % 16) == 0;
+        t.ctas = m[i].ctas;
+        pre = std::min(pre, std::max(1, m[i].nstages - 1));
+    }
+    p.cta_work = cta_work;
+    p.gate = gate;
+    p.nmem = n;
+    p.wide = m[0].d->wide;
+    p.ordered = ordered ? 1 : 0;
+    p.zero_y = zero_y ? 1 : 0;
+    p.pre_tiles = pre;
+    p.trace = trace;
+    const bool coop = coop_launch();
+    const dim3 blk(ecsr::tiled_threads(nc)), grd(grid);
+    if (nc == 8)
+        return lean ? launch_ex(ecsr::ecsr_tiled_kernel<false, 8>, grd, blk, smem, st, coop, p)
+                    : launch_ex(ecsr::ecsr_tiled_kernel<true, 8>, grd, blk, smem, st, coop, p);
+    return lean ? launch_ex(ecsr::ecsr_tiled_kernel<false, 16>, grd, blk, smem, st, coop, p)
+                : launch_ex(ecsr::ecsr_tiled_kernel<true, 16>, grd, blk, smem, st, coop, p);
 }
 
 template <typename T, typename VT, typename XT>
@@ -920,7 +1024,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             d->wide = wide;
             d->stage_bytes = static_cast<int>(stage);
             d->nstages = static_cast<int>(nst);
-            d->smem_bytes = static_cast<int>(round_up(16 * nst + 8, 128) + nst * stage + xbytes);
+            d->smem_bytes = static_cast<int>(round_up(8 * nst + 8, 128) + nst * stage + xbytes);
             const int64_t ntiles = static_cast<int64_t>(tstart.size()) - 1;
             d->ntiles = ntiles;
             const int grid =
@@ -997,16 +1101,20 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 if (d->d_tile_meta) d->allocs.push_back(d->d_tile_meta);
             }
             d->cta_tile_h = scta;
+            d->gate_ok = grid <= usable_sms(lim.sms) * ctas_per_sm;
+            for (double c : tcost) d->total_cost += c;
             std::vector<uint32_t> ranges(2 * grid);
+            std::vector<uint4> work(grid);
             for (int b = 0; b < grid; ++b) {
                 const int r = range_of_block(b, grid, ctas_per_sm);
                 ranges[2 * b] = scta[r];
                 ranges[2 * b + 1] = scta[r + 1];
+                work[b] = make_uint4(0u, scta[r], scta[r + 1], static_cast<uint32_t>(r));
             }
             d->cta_range_h = ranges;
             if (err == cudaSuccess) {
-                d->d_cta_tile = dalloc_copy(ranges, &total, &err);
-                if (d->d_cta_tile) d->allocs.push_back(d->d_cta_tile);
+                d->d_cta_work = dalloc_copy(work, &total, &err);
+                if (d->d_cta_work) d->allocs.push_back(d->d_cta_work);
             }
             if (err != cudaSuccess) {
                 delete d;
@@ -1061,26 +1169,7 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
     DeviceGuard guard(d->device);  // the handle's device, whatever the caller's current one
     ECSR_CUDA(guard.err);
     if (d->layout == 1) {
-        ecsr::TiledParams p;
-        p.arena = d->d_arena;
-        p.tile_meta = reinterpret_cast<const uint2*>(d->d_tile_meta);
-        p.cta_tile = d->d_cta_tile;
-        p.queue = ws->queue;
-        p.queue_begin = d->queue_begin;
-        p.nqueue = d->nqueue;
-        p.x = static_cast<const __half*>(x);
-        p.y = static_cast<float*>(y);
-        p.partials = static_cast<float*>(ws->partials);
-        p.K = static_cast<int32_t>(d->K);
-        p.ordered = ordered ? 1 : 0;
-        p.stage_bytes = d->stage_bytes;
-        p.nstages = d->nstages;
-        p.x_vec16 = (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-        p.pre_tiles = std::min(pre_tiles(), std::max(1, d->nstages - 1));
-        p.sync = ws->sync;
-        p.M = d->M;
-        p.zero_y = (!ordered && !accumulate) ? 1 : 0;
-        p.trace = nullptr;
+        unsigned long long* trace = nullptr;
         if (trace_enabled()) {  // tuning builds only
             ecsr_dev* dm = const_cast<ecsr_dev*>(d);
             if (!dm->d_trace) {
@@ -1093,19 +1182,15 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
                 ECSR_CUDA(cudaMemcpyAsync(dm->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice, st));
                 ECSR_CUDA(cudaStreamSynchronize(st));
             }
-            p.trace = dm->d_trace;
+            trace = dm->d_trace;
         }
-        p.wide = d->wide;
-        const int nc = ecsr::kConsumerWarpsPerSm / d->ctas_per_sm;
-        const dim3 blk(ecsr::tiled_threads(nc)), grd(d->grid);
-        cudaError_t e;
-        if (nc == 8)
-            e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false, 8>, grd, blk, d->smem_bytes, st, p)
-                        : launch_pdl(ecsr::ecsr_tiled_kernel<true, 8>, grd, blk, d->smem_bytes, st, p);
-        else
-            e = d->lean ? launch_pdl(ecsr::ecsr_tiled_kernel<false, 16>, grd, blk, d->smem_bytes, st, p)
-                        : launch_pdl(ecsr::ecsr_tiled_kernel<true, 16>, grd, blk, d->smem_bytes, st, p);
-        ECSR_CUDA(e);
+        // overwrite: zero y inside the kernel (gate) when the whole grid can be resident,
+        // else (or on request) a memset first and an ungated launch
+        const bool memset_y = !ordered && !accumulate && (!d->gate_ok || (mode & ECSR_SPMV_MEMSET_Y));
+        if (memset_y) ECSR_CUDA(cudaMemsetAsync(y, 0, 4 * d->M, st));
+        const MemberLaunch m{d, x, y, ws->queue, ws->partials, d->grid, d->nstages};
+        ECSR_CUDA(launch_tiled(&m, 1, d->d_cta_work, d->grid, ecsr::kConsumerWarpsPerSm / d->ctas_per_sm, d->lean,
+                               d->smem_bytes, ws->gate, ordered, !ordered && !accumulate && !memset_y, trace, st));
         if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, ws->partials, st));
         return ECSR_OK;
     }
@@ -1121,6 +1206,230 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
     else ECSR_CUDA(launch_finish<float>(d, y, accumulate, ws->partials, st));
     return ECSR_OK;
 }
+
+// ---------------------------------------------------------------------------------
+// Grouped launch: several independent products y_i = A_i x_i in ONE tiled launch. Each
+// CTA works on one member (its x, a contiguous run of the member's own cost-balanced
+// tile ranges, its tail queue); members get CTAs in proportion to their tile cost, and
+// co-resident CTAs pair a member's first ranges with another's last. One launch ramp,
+// one x-load latency and one tail are paid for the whole group instead of per matrix.
+// ---------------------------------------------------------------------------------
+struct ecsr_group {
+    // Members packed for two CTAs per SM run in one launch, members packed for one CTA
+    // per SM (x > 32 KB) in a second one (a "part" each), issued back to back.
+    struct Part {
+        std::vector<int> idx;   // members of this launch (group order)
+        std::vector<int> ctas;  // CTAs per member
+        std::vector<int> nst;   // stage-pool depth per member in this launch
+        int grid = 0, nc = 8, smem = 0, cps = 2;
+        bool lean = true, gate_ok = true;
+        uint4* d_cta_work = nullptr;
+        size_t gate_off = 0;    // gate words in each workspace
+    };
+    int device = 0;
+    std::vector<const ecsr_dev*> mats;
+    std::vector<Part> parts;
+    size_t queue_off = 0, ws_bytes = 0;  // member i's queue: queue_off + 128 * i
+    static constexpr int kStreamSlots = 4;
+    uint8_t* ws_base = nullptr;          // kStreamSlots workspaces of ws_bytes
+    mutable cudaStream_t ws_stream[kStreamSlots] = {};
+    mutable int ws_bound = 0;
+    mutable std::mutex ws_mu;
+    std::vector<void*> allocs;
+    uint8_t* workspace(cudaStream_t stream) const {
+        std::lock_guard<std::mutex> lock(ws_mu);
+        for (int i = 0; i < ws_bound; ++i)
+            if (ws_stream[i] == stream) return ws_base + ws_bytes * i;
+        if (ws_bound == kStreamSlots) return nullptr;
+        ws_stream[ws_bound] = stream;
+        return ws_base + ws_bytes * ws_bound++;
+    }
+    ~ecsr_group() {
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+// Plan one launch over members `idx` at `cps` CTAs per SM: CTAs per member in proportion
+// to tile cost (at least 1, at most the member's static range count), member i's j-th
+// CTA merging its static ranges [j R / c, (j + 1) R / c) (contiguous in the arena, equal
+// cost each); co-resident CTAs pair one member's first ranges with another's last.
+int plan_part(const std::vector<const ecsr_dev*>& mats, const DeviceLimits& lim, ecsr_group::Part* pt,
+              std::vector<uint4>* work) {
+    const int n = static_cast<int>(pt->idx.size());
+    pt->nc = ecsr::kConsumerWarpsPerSm / pt->cps;
+    int64_t cap = 0;
+    double total = 0;
+    for (int i : pt->idx) {
+        const ecsr_dev* d = mats[i];
+        int nst = d->nstages, smem = d->smem_bytes;
+        if (d->ctas_per_sm != pt->cps) {  // a two-CTA member in a one-CTA launch: deepen its pool
+            const int64_t xbytes = round_up(2 * std::max<int64_t>(d->K, 1), 16);
+            const int64_t avail = lim.smem_optin - 4096 - 16 * kMaxStages - xbytes;
+            nst = static_cast<int>(std::min<int64_t>(kMaxStages, avail / std::max(d->stage_bytes, 1)));
+            smem = static_cast<int>(round_up(8 * nst + 8, 128) + int64_t{nst} * d->stage_bytes + xbytes);
+        }
+        pt->nst.push_back(nst);
+        pt->smem = std::max(pt->smem, smem);
+        pt->lean = pt->lean && d->lean;
+        cap += d->grid;
+        total += d->total_cost;
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(int64_t{lim.sms} * pt->cps, cap));
+    std::vector<int> c(n, 1);
+    int used = n;
+    while (used < grid) {
+        int best = -1;
+        double deficit = -1e300;
+        for (int k = 0; k < n; ++k) {
+            const ecsr_dev* d = mats[pt->idx[k]];
+            if (c[k] >= d->grid) continue;
+            const double want = grid * d->total_cost / std::max(total, 1e-30);
+            if (want - c[k] > deficit) {
+                deficit = want - c[k];
+                best = k;
+            }
+        }
+        if (best < 0) break;
+        ++c[best];
+        ++used;
+    }
+    pt->grid = used;
+    pt->ctas = c;
+    pt->gate_ok = pt->grid <= usable_sms(lim.sms) * pt->cps;
+    std::vector<uint4> jobs;
+    for (int k = 0; k < n; ++k) {
+        const ecsr_dev* d = mats[pt->idx[k]];
+        const int R = d->grid;
+        for (int j = 0; j < c[k]; ++j) {
+            const int r0 = static_cast<int>(static_cast<int64_t>(j) * R / c[k]);
+            const int r1 = static_cast<int>(static_cast<int64_t>(j + 1) * R / c[k]);
+            jobs.push_back(make_uint4(static_cast<uint32_t>(k), d->cta_tile_h[r0], d->cta_tile_h[r1],
+                                      static_cast<uint32_t>(j)));
+        }
+    }
+    work->assign(pt->grid, make_uint4(0, 0, 0, 0));
+    for (int b = 0; b < pt->grid; ++b) (*work)[b] = jobs[range_of_block(b, pt->grid, pt->cps)];
+    return ECSR_OK;
+}
+
+}  // namespace
+
+int ecsr_b200_group_create(const ecsr_dev* const* mats, int32_t n, ecsr_group** out) {
+    if (!out) return fail(ECSR_ERR_VALUE, "out is null");
+    *out = nullptr;
+    if (!mats || n < 1 || n > ecsr::kMaxMembers)
+        return fail(ECSR_ERR_VALUE, "a group holds 1 to " + std::to_string(ecsr::kMaxMembers) + " matrices");
+    for (int i = 0; i < n; ++i) {
+        const ecsr_dev* d = mats[i];
+        if (!d) return fail(ECSR_ERR_VALUE, "null handle in group");
+        if (d->layout != 1 || d->M == 0 || d->grid == 0)
+            return fail(ECSR_ERR_VALUE, "group members must use the tiled layout (fp16, W = 32, B <= 8)");
+        if (d->device != mats[0]->device) return fail(ECSR_ERR_VALUE, "group members on different devices");
+        if (d->wide != mats[0]->wide)
+            return fail(ECSR_ERR_VALUE, "group members must all have K <= 65535 or all K > 65535");
+    }
+    DeviceLimits lim;
+    int rc = query_limits(mats[0]->device, &lim);
+    if (rc) return rc;
+    auto* g = new ecsr_group();
+    g->device = mats[0]->device;
+    g->mats.assign(mats, mats + n);
+    for (int cps : {2, 1}) {
+        ecsr_group::Part pt;
+        pt.cps = cps;
+        for (int i = 0; i < n; ++i)
+            if ((group_force_cps1() ? 1 : mats[i]->ctas_per_sm) == cps) pt.idx.push_back(i);
+        if (!pt.idx.empty()) g->parts.push_back(pt);
+    }
+    DeviceGuard guard(g->device);
+    if (guard.err != cudaSuccess) {
+        delete g;
+        return fail(ECSR_ERR_CUDA, cudaGetErrorString(guard.err));
+    }
+    size_t off = 0;
+    for (auto& pt : g->parts) {
+        std::vector<uint4> work;
+        plan_part(g->mats, lim, &pt, &work);
+        int64_t total_bytes = 0;
+        cudaError_t err = cudaSuccess;
+        pt.d_cta_work = dalloc_copy(work, &total_bytes, &err);
+        if (pt.d_cta_work) g->allocs.push_back(pt.d_cta_work);
+        if (err == cudaSuccess) rc = configure_tiled_kernels(g->device, pt.smem);
+        else rc = fail(ECSR_ERR_CUDA, std::string("group schedule: ") + cudaGetErrorString(err));
+        if (rc) {
+            delete g;
+            return rc;
+        }
+        pt.gate_off = off;
+        off += gate_bytes(pt.grid);
+    }
+    g->queue_off = off;
+    g->ws_bytes = off + 128 * static_cast<size_t>(n);
+    cudaError_t err = cudaMalloc(&g->ws_base, g->ws_bytes * ecsr_group::kStreamSlots);
+    if (g->ws_base) g->allocs.push_back(g->ws_base);
+    if (err == cudaSuccess) err = cudaMemset(g->ws_base, 0, g->ws_bytes * ecsr_group::kStreamSlots);
+    if (err != cudaSuccess) {
+        delete g;
+        return fail(ECSR_ERR_CUDA, std::string("group workspace: ") + cudaGetErrorString(err));
+    }
+    *out = g;
+    return ECSR_OK;
+}
+
+int ecsr_b200_group_spmv(const ecsr_group* g, const void* const* xs, void* const* ys, int32_t mode,
+                         void* stream) {
+    if (!g || !xs || !ys) return fail(ECSR_ERR_VALUE, "null argument");
+    const int n = static_cast<int>(g->mats.size());
+    for (int i = 0; i < n; ++i)
+        if (!xs[i] || !ys[i]) return fail(ECSR_ERR_VALUE, "null x or y");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (mode & ECSR_SPMV_ORDERED) {  // bitwise mode: the members one after another
+        for (int i = 0; i < n; ++i) {
+            const int rc = ecsr_b200_spmv(g->mats[i], xs[i], ys[i], mode, stream);
+            if (rc) return rc;
+        }
+        return ECSR_OK;
+    }
+    uint8_t* ws = g->workspace(st);
+    if (!ws)
+        return fail(ECSR_ERR_VALUE, "group already used from " + std::to_string(ecsr_group::kStreamSlots) +
+                                        " other streams (one workspace per stream)");
+    DeviceGuard guard(g->device);
+    ECSR_CUDA(guard.err);
+    for (const auto& pt : g->parts) {
+        MemberLaunch m[ecsr::kMaxMembers];
+        const int k = static_cast<int>(pt.idx.size());
+        for (int j = 0; j < k; ++j) {
+            const int i = pt.idx[j];
+            m[j] = MemberLaunch{g->mats[i], xs[i], ys[i], reinterpret_cast<uint32_t*>(ws + g->queue_off + 128 * i),
+                                nullptr, pt.ctas[j], pt.nst[j]};
+        }
+        const bool overwrite = (mode & ECSR_SPMV_ACCUMULATE) == 0;
+        const bool memset_y = overwrite && (!pt.gate_ok || (mode & ECSR_SPMV_MEMSET_Y));
+        if (memset_y)
+            for (int j = 0; j < k; ++j) ECSR_CUDA(cudaMemsetAsync(m[j].y, 0, 4 * m[j].d->M, st));
+        ECSR_CUDA(launch_tiled(m, k, pt.d_cta_work, pt.grid, pt.nc, pt.lean, pt.smem,
+                               reinterpret_cast<unsigned long long*>(ws + pt.gate_off), false,
+                               overwrite && !memset_y, nullptr, st));
+    }
+    return ECSR_OK;
+}
+
+int ecsr_b200_group_info(const ecsr_group* g, int32_t* launches, int32_t* grid, int32_t* ctas, int32_t n) {
+    if (!g) return fail(ECSR_ERR_VALUE, "null group");
+    if (launches) *launches = static_cast<int32_t>(g->parts.size());
+    if (grid) *grid = 0;
+    for (const auto& pt : g->parts) {
+        if (grid) *grid += pt.grid;
+        for (size_t j = 0; j < pt.idx.size(); ++j)
+            if (ctas && pt.idx[j] < n) ctas[pt.idx[j]] = pt.ctas[j];
+    }
+    return ECSR_OK;
+}
+
+void ecsr_b200_group_free(ecsr_group* g) { delete g; }
 
 int ecsr_b200_info(const ecsr_dev* d, int64_t* num_rows, int64_t* num_cols, int32_t* nsets,
                    int32_t* warp_size, int32_t* delta_bits, int32_t* value_bits, int32_t* device_dtype) {
@@ -1302,6 +1611,142 @@ int ecsr_b200_unpack(const ecsr_dev* d, ecsr_out_set* out, int32_t nsets, int32_
         }
         voff += sd.stored * sd.g;
     }
+    return ECSR_OK;
+}
+
+// Access trace of the device layout (the reference's
+// spmv_ec_traced + check_coalescing, executor.py:106-221): one entry per block, warp
+// step and array, in the order the kernel issues the shared-memory reads, each mapped
+// back to the reference array span it carries. The tiled walk replays the kernel's
+// own pointer arithmetic (tiled_group_record / tiled_wide_record in ecsr_kernels.cuh),
+// not unpack's, so the audit checks the addresses the kernel really reads.
+int ecsr_b200_trace(const ecsr_dev* d, ecsr_trace_rec* out, int64_t cap, int64_t* count) {
+    if (!d || !count) return fail(ECSR_ERR_VALUE, "null argument");
+    const int nsets = static_cast<int>(d->sets.size());
+    std::vector<int64_t> warp0(nsets + 1, 0);
+    for (int si = 0; si < nsets; ++si) warp0[si + 1] = warp0[si] + d->sets[si].nb;
+    int64_t n = 0;
+    auto emit = [&](int64_t warp, int32_t step, int32_t array, int32_t set, int32_t lane_bytes, int64_t start,
+                    int64_t span, int64_t dev_offset, int64_t dev_bytes) {
+        if (out && n < cap)
+            out[n] = ecsr_trace_rec{warp, step, array, set, lane_bytes, start, span, dev_offset, dev_bytes};
+        ++n;
+    };
+    if (d->layout == 2) {  // generic kernel: the reference arrays, element loads per lane
+        const int esz = elem_size(d->dtype);
+        for (int si = 0; si < nsets; ++si) {
+            const SetDesc& sd = d->sets[si];
+            std::vector<int64_t> indptr(sd.nb + 1);
+            ECSR_CUDA(cudaMemcpy(indptr.data(), d->d_indptr + sd.indptr_off, 8 * (sd.nb + 1), cudaMemcpyDeviceToHost));
+            const int64_t chunk = static_cast<int64_t>(d->W) * sd.v;
+            for (int64_t b = 0; b < sd.nb; ++b)
+                for (int64_t c = 0; c < (indptr[b + 1] - indptr[b]) / chunk; ++c) {
+                    const int64_t st = indptr[b] + c * chunk;
+                    emit(warp0[si] + b, static_cast<int32_t>(c), 0, si, 4, st, chunk, 4 * (sd.col_off + st), 4 * chunk);
+                    emit(warp0[si] + b, static_cast<int32_t>(c), 1, si, esz, st * sd.g, chunk * sd.g,
+                         esz * (sd.val_off + st * sd.g), esz * chunk * sd.g);
+                }
+        }
+        *count = n;
+        return ECSR_OK;
+    }
+    std::vector<uint8_t> arena(d->arena_bytes);
+    std::vector<uint32_t> tstart(d->ntiles + 1);
+    ECSR_CUDA(cudaMemcpy(arena.data(), d->d_arena, d->arena_bytes, cudaMemcpyDeviceToHost));
+    ECSR_CUDA(cudaMemcpy(tstart.data(), d->d_tile_start16, 4 * (d->ntiles + 1), cudaMemcpyDeviceToHost));
+    // pass 1: chunk count of every block -> the reference's block_indptr (in chunks)
+    std::vector<std::vector<int64_t>> nch(nsets);
+    for (int si = 0; si < nsets; ++si) nch[si].assign(d->sets[si].nb, -1);
+    auto locate = [&](uint32_t slot, int g, int* set, int64_t* blk) -> bool {
+        for (int si = nsets - 1; si >= 0; --si) {
+            const SetDesc& sd = d->sets[si];
+            if (sd.nb == 0 || sd.slot0 > slot) continue;
+            if (sd.g != g) return false;
+            *set = si;
+            *blk = (static_cast<int64_t>(slot) - sd.slot0) / g;
+            return *blk < sd.nb;
+        }
+        return false;
+    };
+    for (int64_t t = 0; t < d->ntiles; ++t) {
+        const uint8_t* tile = arena.data() + 16ull * tstart[t];
+        uint32_t nrec;
+        std::memcpy(&nrec, tile, 4);
+        for (uint32_t jr = 0; jr < nrec; ++jr) {
+            uint16_t off16, nmin;
+            std::memcpy(&off16, tile + 8 + 2 * jr, 2);
+            const uint8_t* r = tile + 16 * off16;
+            std::memcpy(&nmin, r + 48, 2);
+            for (int bk = 0; bk < r[52]; ++bk) {
+                uint32_t slot;
+                uint16_t nt;
+                std::memcpy(&slot, r + 4 * bk, 4);
+                std::memcpy(&nt, r + 32 + 2 * bk, 2);
+                int si;
+                int64_t blk;
+                if (!locate(slot, r[50], &si, &blk) || nch[si][blk] >= 0)
+                    return fail(ECSR_ERR_CONTAINER, "record slot outside every set or repeated");
+                nch[si][blk] = static_cast<int64_t>(nmin) + nt;
+            }
+        }
+    }
+    std::vector<std::vector<int64_t>> first(nsets);  // stored column of each block's chunk 0
+    for (int si = 0; si < nsets; ++si) {
+        const SetDesc& sd = d->sets[si];
+        first[si].assign(sd.nb, 0);
+        int64_t acc = 0;
+        for (int64_t b = 0; b < sd.nb; ++b) {
+            if (nch[si][b] < 0) return fail(ECSR_ERR_CONTAINER, "arena holds fewer blocks than sets");
+            first[si][b] = acc;
+            acc += nch[si][b] * 32 * sd.v;
+        }
+    }
+    // pass 2: the kernel's walk
+    const int64_t bases = d->wide ? 128 : 64;  // lane bases per block, bytes
+    for (int64_t t = 0; t < d->ntiles; ++t) {
+        const int64_t tile = 16ll * tstart[t];
+        uint32_t nrec;
+        std::memcpy(&nrec, arena.data() + tile, 4);
+        for (uint32_t jr = 0; jr < nrec; ++jr) {
+            uint16_t off16, nmin;
+            std::memcpy(&off16, arena.data() + tile + 8 + 2 * jr, 2);
+            const int64_t r = tile + 16 * off16;
+            const uint8_t* rh = arena.data() + r;
+            std::memcpy(&nmin, rh + 48, 2);
+            const int g = rh[50], v = rh[51], nb = rh[52], P = rh[54];
+            int sb[8];
+            int64_t bb[8];
+            for (int bk = 0; bk < nb; ++bk) {
+                uint32_t slot;
+                std::memcpy(&slot, rh + 4 * bk, 4);
+                locate(slot, g, &sb[bk], &bb[bk]);
+            }
+            const int64_t dch = 32 * v;
+            auto chunk = [&](int bk, int64_t c, int64_t dptr, int64_t vptr, int64_t vbytes) {
+                const int si = sb[bk];
+                const int64_t st = first[si][bb[bk]] + c * dch;
+                emit(warp0[si] + bb[bk], static_cast<int32_t>(c), 0, si, v, st, dch, dptr, dch);
+                emit(warp0[si] + bb[bk], static_cast<int32_t>(c), 1, si, g > 8 ? 16 : 2 * v * g, st * g, dch * g,
+                     vptr, vbytes);
+            };
+            if (g <= 8) {  // tiled_group_record<G, V, P>
+                const int64_t vch = 64 * v * g;
+                int64_t ptr = r + ecsr::group_header_bytes(g, P) + bases * P;
+                for (int64_t c = 0; c < nmin; ++c, ptr += P * (dch + vch))
+                    for (int bk = 0; bk < nb; ++bk) chunk(bk, c, ptr + bk * dch, ptr + P * dch + bk * vch, vch);
+                for (int bk = 0; bk < nb; ++bk) {
+                    uint16_t nt;
+                    std::memcpy(&nt, rh + 32 + 2 * bk, 2);
+                    for (int64_t c = 0; c < nt; ++c, ptr += dch + vch) chunk(bk, nmin + c, ptr, ptr + dch, vch);
+                }
+            } else {  // tiled_wide_record<V>: one block, g / 8 passes over the same spans
+                const int64_t vch = 64ll * v * g;
+                int64_t ptr = r + ecsr::group_header_bytes(g, 1) + bases;
+                for (int64_t c = 0; c < nmin; ++c, ptr += dch + vch) chunk(0, c, ptr, ptr + dch, vch);
+            }
+        }
+    }
+    *count = n;
     return ECSR_OK;
 }
 

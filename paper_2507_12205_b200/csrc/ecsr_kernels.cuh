@@ -41,29 +41,49 @@ namespace ecsr {
 constexpr int kConsumerWarpsPerSm = 16;
 __host__ __device__ constexpr int tiled_threads(int nc) { return 32 * (nc + 1); }
 constexpr int kMaxRingStages = 16;
-constexpr int kTickets = 3;  // tail-queue tickets a producer keeps in flight
+constexpr int kTickets = 3;     // tail-queue tickets a producer keeps in flight
+constexpr int kMaxMembers = 8;  // matrices of one grouped launch
 
-struct TiledParams {
-    const uint8_t* arena;          // block-major tiles, 16-B aligned
+// One matrix of a (grouped) launch: its packed arena and this launch's x and y.
+struct TiledMember {
+    const uint8_t* arena;          // tiles, 16-B aligned
     const uint2* tile_meta;        // [ntiles] {start16, nrec | bytes16 << 16}
-    const uint32_t* cta_tile;      // [2 * grid] static tile range [lo, hi) of each CTA
-    uint32_t* queue;               // [2] tail queue {next tile, CTAs done} (per-stream workspace)
-    uint32_t queue_begin;          // tiles [queue_begin, queue_begin + nqueue) go through the queue
-    uint32_t nqueue;
     const __half* x;               // [K]
     float* y;                      // [M]
     float* partials;               // [nslots] (ordered mode)
+    uint32_t* queue;               // [2] tail queue {next tile, CTAs done} (per-stream workspace)
+    int64_t M;
+    uint32_t queue_begin;          // tiles [queue_begin, queue_begin + nqueue) go through the queue
+    uint32_t nqueue;
     int32_t K;
-    int32_t ordered;
     int32_t stage_bytes;
     int32_t nstages;
-    unsigned long long* sync;      // grid-barrier generation counter (zero_y mode)
-    int64_t M;
     int32_t x_vec16;               // x is 16-B aligned
+    int32_t ctas;                  // CTAs of the launch working on this matrix
+};
+
+// Zero-y gate workspace (per stream): one 64-bit counter of zeroed slices, on its own
+// 128-B line. A launch of `grid` CTAs adds exactly `grid` to it.
+constexpr int kGateWords = 16;
+
+struct TiledParams {
+    TiledMember mem[kMaxMembers];
+    const uint4* cta_work;         // [grid] {member, tile lo, tile hi, slice index in member}
+    unsigned long long* gate;      // zero-y gate workspace (zero_y mode)
+    int32_t nmem;
+    int32_t ordered;
+    int32_t wide;                  // K > 65535 (every member): u32 bases (else u16)
     int32_t zero_y;                // overwrite: the kernel zeroes y itself (no memset launch)
-    int32_t wide;                  // K > 65535: u32 bases (else u16)
     int32_t pre_tiles;             // tiles streamed before griddepcontrol.wait / x
     unsigned long long* trace;     // tuning builds: per-CTA timeline [grid][16] or null
+};
+
+// What a record needs: its member's outputs (registers) and the launch-wide flags,
+// read from the kernel parameters so they stay uniform (uniform branches).
+struct RecCtx {
+    float* y;
+    float* partials;
+    const TiledParams* tp;
 };
 
 // ---------------------------------------------------------------------------------
@@ -224,44 +244,100 @@ __host__ __device__ constexpr int header_bytes() {
     return (8 + 4 * G + 15) & ~15;
 }
 
-// Per-warp state of the zero-y grid barrier: REDs into y may only start once every
-// CTA has zeroed its slice of y (see ecsr_tiled_kernel).
-// The CTA's arrival (producer warp) publishes target + 1 in shared memory
-// (`target_smem`, 0 = not yet). The first consumer warp of the CTA to reach the gate
-// (shared `state` 0 -> 1) polls the grid counter with acquire loads and then releases
-// state = 2 at CTA scope; the other warps only watch the shared word, so a CTA pays
-// one loaded-L2 round trip instead of one per warp.
+// Zero-y gate (overwrite mode without a memset launch): every slice of y -- one per CTA
+// of the launch: rows [M*i/ctas, M*(i+1)/ctas) of the CTA's member -- must be zeroed
+// before any red.global.add into y. Each CTA's producer zeroes its slice after
+// griddepcontrol.wait and adds 1 to the gate counter (release); the counter's old value
+// gives the launch's target (the next multiple of the grid). The first consumer warp of
+// a CTA to reach the gate polls the counter (acquire) and opens the gate for the others
+// (a CTA-scope release/acquire flag; atomics, so racecheck sees synchronised accesses).
+// Every CTA of the grid must be able to be resident at once: the launcher checks that
+// against the SMs this context may use (green-context SM partitions, the MPS active
+// thread percentage) and otherwise clears y with a memset and launches without the gate.
+// Measured alternative (round 2): per-slice claims that let resident CTAs zero absent
+// CTAs' slices cost an extra atomic round trip per CTA near launch start, where atomics
+// queue behind the bulk tile copies (~1-5 us), i.e. 3-10 % of the step.
+__device__ __forceinline__ uint32_t atom_load_cta(const uint32_t* a) {
+    uint32_t v;
+    asm volatile("atom.acquire.cta.shared.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(smem_addr(a)) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long atom_load_cta64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("atom.acquire.cta.shared.or.b64 %0, [%1], 0;" : "=l"(v) : "r"(smem_addr(a)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void atom_store_cta64(unsigned long long* a, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.release.cta.shared.exch.b64 %0, [%1], %2;" : "=l"(old) : "r"(smem_addr(a)), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
+    const uint32_t lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(v), src);
+    const uint32_t hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+// Zero the slice of y that CTA work item `w` owns, with `n` lanes starting at `l`.
+__device__ __forceinline__ void zero_slice(const TiledParams& p, const uint4& w, int l, int n) {
+    const TiledMember& m = p.mem[w.x];
+    const int64_t r0 = m.M * w.w / m.ctas, r1 = m.M * (w.w + 1) / m.ctas;
+    for (int64_t r = r0 + l; r < r1; r += n) m.y[r] = 0.0f;
+}
+
+// The closed-gate path: out of line, so the ~20 record variants that inline pass() stay
+// small (instruction cache).
+__device__ __noinline__ void ygate_wait(const TiledParams* p, unsigned long long* target_smem, uint32_t* state,
+                                        int lane);
+
 struct YGate {
-    const unsigned long long* counter;
-    const unsigned long long* target_smem;
-    uint32_t* state;
+    const TiledParams* p;
+    unsigned long long* target_smem;  // counter target + 1, published by the producer
+    uint32_t* state;                  // 0 closed, 1 a warp polls, 2 open
     bool open;
     __device__ __forceinline__ void pass(int lane) {
+#ifdef ECSR_EXP_NO_GATE  // timing experiment only: y is NOT correct
+        return;
+#endif
         if (open) return;
-        if (lane == 0) {
-            uint32_t st = atomicCAS(state, 0u, 1u);
-            if (st == 0u) {
-                unsigned long long tgt;
-                do {
-                    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(tgt) : "r"(smem_addr(target_smem)) : "memory");
-                } while (tgt == 0);
-                --tgt;
-                unsigned long long v;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
-                } while (static_cast<long long>(v - tgt) < 0);
-                asm volatile("st.release.cta.shared.u32 [%0], 2;" ::"r"(smem_addr(state)) : "memory");
-            } else {
-                while (st != 2u) {
-                    __nanosleep(32);
-                    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(st) : "r"(smem_addr(state)) : "memory");
-                }
-            }
-        }
-        __syncwarp();
+        ygate_wait(p, target_smem, state, lane);
         open = true;
     }
 };
+
+__device__ __noinline__ void ygate_wait(const TiledParams* p, unsigned long long* target_smem, uint32_t* state,
+                                        int lane) {
+    {
+        uint32_t st = 0;
+        if (lane == 0) st = atomicCAS(state, 0u, 1u);
+        st = __shfl_sync(0xffffffffu, st, 0);
+        if (st == 0) {  // this warp polls the grid counter for the CTA
+            unsigned long long tgt = 0;  // target + 1, once the producer published it
+            if (lane == 0)
+                do {
+                    tgt = atom_load_cta64(target_smem);
+                } while (tgt == 0);
+            if (lane == 0) {
+                --tgt;
+                unsigned long long v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p->gate) : "memory");
+                } while (static_cast<long long>(v - tgt) < 0);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                uint32_t old;
+                asm volatile("atom.release.cta.shared.exch.b32 %0, [%1], 2;" : "=r"(old) : "r"(smem_addr(state)) : "memory");
+                if (p->trace) p->trace[blockIdx.x * 16 + 14] = gtimer();  // tuning builds: gate open
+            }
+        } else if (lane == 0) {
+            while (st != 2u) {
+                __nanosleep(32);
+                st = atom_load_cta(state);
+            }
+        }
+        __syncwarp();
+    }
+}
 
 // Group records (packer: ecsr_b200.cu, build_tiled_arena / write_group_record): P = 8/g
 // consecutive blocks (P = 1 for g >= 8) whose chunk streams are interleaved, so a warp
@@ -323,8 +399,8 @@ __device__ __forceinline__ void chunk_fma(const uint32_t (&d)[(V + 3) / 4], cons
 // Emit one row sum: red.global.add.f32 into y (fast) or the block's partial slot
 // (ordered; summed per row in container order by ecsr_finish_rows).
 __device__ __forceinline__ void emit_row(uint32_t r, int g, int P, int blk, int k, float sum,
-                                         const TiledParams& p) {
-    if (p.ordered) {
+                                         const RecCtx& p) {
+    if (p.tp->ordered) {
         uint32_t slot;
         lds_bytes<4>(r + 4 * blk, &slot);
         asm volatile("st.global.f32 [%0], %1;" ::"l"(p.partials + slot + k), "f"(sum) : "memory");
@@ -339,9 +415,11 @@ __device__ __forceinline__ void emit_row(uint32_t r, int g, int P, int blk, int 
 // accumulates its segment sequentially (reference order); the 8 accumulators then
 // share one butterfly reduce-scatter whose per-accumulator association is the
 // reference's lane tree (_speedups.pyx:120-127).
-template <int G, int V, int P>
-__device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const TiledParams& p,
-                                                   YGate& gate) {
+// `next` runs once per record, right before the lane reduction: the consumer loop claims
+// its next record there, so the claim's round trip overlaps the shuffles.
+template <int G, int V, int P, class Next>
+__device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const RecCtx& p,
+                                                   YGate& gate, Next&& next) {
     constexpr int NACC = P * G;
     constexpr int kStride = 32 / NACC;
     const int a = lane / kStride;  // accumulator a after the reduce-scatter: block a / G, row a % G
@@ -352,9 +430,9 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
     uint32_t m[2];
     lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
     uint32_t out_idx;
-    lds_bytes<4>(p.ordered ? r + 4 * blk : r + 64 + 4 * (blk * G + k), &out_idx);
+    lds_bytes<4>(p.tp->ordered ? r + 4 * blk : r + 64 + 4 * (blk * G + k), &out_idx);
     uint32_t xa[P];
-    if (p.wide) {
+    if (p.tp->wide) {
         uint32_t bb[P];
         lds_bytes<4 * P>(q + lane * 4 * P, bb);
 #pragma unroll
@@ -366,11 +444,14 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
         for (int b = 0; b < P; ++b) xa[b] = xs + 2u * ((bb[b >> 1] >> (16 * (b & 1))) & 0xffffu);
     }
     const uint32_t nmin = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
-    if (!present) return;  // zero-width blocks only (_speedups.pyx:105-106)
+    if (!present) {  // zero-width blocks only (_speedups.pyx:105-106)
+        next();
+        return;
+    }
     const bool has_tail = (m[1] >> 24) != 0;  // header byte 55
     constexpr uint32_t DCH = 32 * V, VCH = 64 * V * G, LV = 2 * V * G;  // bytes
     constexpr int NW = (LV + 3) / 4;
-    uint32_t ptr = q + (p.wide ? 128u : 64u) * P;
+    uint32_t ptr = q + (p.tp->wide ? 128u : 64u) * P;
     float acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0f;
@@ -407,10 +488,11 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
             }
         }
     }
+    next();
     const float sum = warp_reduce_scatter<NACC>(acc, lane);
-    if (!p.ordered) gate.pass(lane);
+    if (!p.tp->ordered) gate.pass(lane);
     if ((lane & (kStride - 1)) == 0 && ((present >> blk) & 1u)) {
-        if (p.ordered)
+        if (p.tp->ordered)
             asm volatile("st.global.f32 [%0], %1;" ::"l"(p.partials + out_idx + k), "f"(sum) : "memory");
         else
             asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p.y + out_idx), "f"(sum) : "memory");
@@ -419,24 +501,25 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
 
 // A single-block record of g = 8 * passes rows (g in {16, 32}): one walk per pass of
 // 8 rows; a column's g values are contiguous, so a pass reads one 16-byte slice.
-template <int V>
+template <int V, class Next>
 __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs, int lane,
-                                                  const TiledParams& p, YGate& gate) {
+                                                  const RecCtx& p, YGate& gate, Next&& next) {
     constexpr int G = 8;
     uint32_t m[2];
     lds_bytes<8>(r + 48, m);
+    next();
     const uint32_t nch = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
     if (!present) return;
     const uint32_t q = r + group_header_bytes(g, 1);
     uint32_t base;
-    if (p.wide) lds_bytes<4>(q + lane * 4, &base);
+    if (p.tp->wide) lds_bytes<4>(q + lane * 4, &base);
     else {
         lds_bytes<2>(q + lane * 2, &base);
         base &= 0xffffu;
     }
     constexpr uint32_t DCH = 32 * V;
     const uint32_t vch = 64u * V * g;
-    const uint32_t body = q + (p.wide ? 128u : 64u);
+    const uint32_t body = q + (p.tp->wide ? 128u : 64u);
     for (int pass = 0; pass < g / G; ++pass) {
         uint32_t xa = xs + 2u * base;
         float acc[G];
@@ -458,7 +541,7 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
             }
         }
         const float sum = warp_reduce_scatter<G>(acc, lane);
-        if (!p.ordered) gate.pass(lane);
+        if (!p.tp->ordered) gate.pass(lane);
         if ((lane & 3) == 0) emit_row(r, g, 1, 0, (lane >> 2) + G * pass, sum, p);
     }
 }
@@ -466,82 +549,77 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
 // kFull: every (g, v, P) record variant; otherwise only the common ones (v = 4 with
 // the default P, or half of it for g = 2, or down to a quarter for g = 1; v = 1 with g = 1) -- a smaller kernel body keeps the instruction
 // cache warm; the packer picks the lean kernel when the container needs nothing else.
-template <bool kFull>
+template <bool kFull, class Next>
 __device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P, uint32_t xs, int lane,
-                                             const TiledParams& p, YGate& gate) {
+                                             const RecCtx& p, YGate& gate, Next&& next) {
     const int g = static_cast<int>(gv >> 8);
     const bool v4 = (gv & 0xffu) == 4;
     if constexpr (!kFull) {
         if (!v4) {
-            tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate);
+            tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate, next);
             return;
         }
         switch (g) {
             case 1:
-                if (P == group_blocks(1)) tiled_group_record<1, 4, group_blocks(1)>(r, xs, lane, p, gate);
-                else if (P == group_blocks(1) / 2) tiled_group_record<1, 4, group_blocks(1) / 2>(r, xs, lane, p, gate);
-                else tiled_group_record<1, 4, group_blocks(1) / 4>(r, xs, lane, p, gate);
+                if (P == group_blocks(1)) tiled_group_record<1, 4, group_blocks(1)>(r, xs, lane, p, gate, next);
+                else if (P == group_blocks(1) / 2) tiled_group_record<1, 4, group_blocks(1) / 2>(r, xs, lane, p, gate, next);
+                else tiled_group_record<1, 4, group_blocks(1) / 4>(r, xs, lane, p, gate, next);
                 break;
             case 2:
-                if (P == group_blocks(2)) tiled_group_record<2, 4, group_blocks(2)>(r, xs, lane, p, gate);
-                else tiled_group_record<2, 4, group_blocks(2) / 2>(r, xs, lane, p, gate);
+                if (P == group_blocks(2)) tiled_group_record<2, 4, group_blocks(2)>(r, xs, lane, p, gate, next);
+                else tiled_group_record<2, 4, group_blocks(2) / 2>(r, xs, lane, p, gate, next);
                 break;
-            case 4: tiled_group_record<4, 4, group_blocks(4)>(r, xs, lane, p, gate); break;
-            default: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate); break;
+            case 4: tiled_group_record<4, 4, group_blocks(4)>(r, xs, lane, p, gate, next); break;
+            default: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate, next); break;
         }
         return;
     }
     if (!v4) {  // short 1-grained sets (v = 1, storage.py:99-122) and other narrow blocks
-        if (g == 1) tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate);
-        else if (g == 2) tiled_group_record<2, 1, group_blocks(2)>(r, xs, lane, p, gate);
-        else if (g == 4) tiled_group_record<4, 1, group_blocks(4)>(r, xs, lane, p, gate);
-        else if (g == 8) tiled_group_record<8, 1, 1>(r, xs, lane, p, gate);
-        else tiled_wide_record<1>(r, g, xs, lane, p, gate);
+        if (g == 1) tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate, next);
+        else if (g == 2) tiled_group_record<2, 1, group_blocks(2)>(r, xs, lane, p, gate, next);
+        else if (g == 4) tiled_group_record<4, 1, group_blocks(4)>(r, xs, lane, p, gate, next);
+        else if (g == 8) tiled_group_record<8, 1, 1>(r, xs, lane, p, gate, next);
+        else tiled_wide_record<1>(r, g, xs, lane, p, gate, next);
         return;
     }
     switch ((g << 4) | P) {  // (g, blocks per record) of this run (packer: kRecordCap)
-        case (1 << 4) | 8: tiled_group_record<1, 4, 8>(r, xs, lane, p, gate); break;
-        case (1 << 4) | 4: tiled_group_record<1, 4, 4>(r, xs, lane, p, gate); break;
-        case (1 << 4) | 2: tiled_group_record<1, 4, 2>(r, xs, lane, p, gate); break;
-        case (1 << 4) | 1: tiled_group_record<1, 4, 1>(r, xs, lane, p, gate); break;
-        case (2 << 4) | 4: tiled_group_record<2, 4, 4>(r, xs, lane, p, gate); break;
-        case (2 << 4) | 2: tiled_group_record<2, 4, 2>(r, xs, lane, p, gate); break;
-        case (2 << 4) | 1: tiled_group_record<2, 4, 1>(r, xs, lane, p, gate); break;
-        case (4 << 4) | 2: tiled_group_record<4, 4, 2>(r, xs, lane, p, gate); break;
-        case (4 << 4) | 1: tiled_group_record<4, 4, 1>(r, xs, lane, p, gate); break;
-        case (8 << 4) | 1: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate); break;
-        default: tiled_wide_record<4>(r, g, xs, lane, p, gate); break;  // g = 16, 32
+        case (1 << 4) | 8: tiled_group_record<1, 4, 8>(r, xs, lane, p, gate, next); break;
+        case (1 << 4) | 4: tiled_group_record<1, 4, 4>(r, xs, lane, p, gate, next); break;
+        case (1 << 4) | 2: tiled_group_record<1, 4, 2>(r, xs, lane, p, gate, next); break;
+        case (1 << 4) | 1: tiled_group_record<1, 4, 1>(r, xs, lane, p, gate, next); break;
+        case (2 << 4) | 4: tiled_group_record<2, 4, 4>(r, xs, lane, p, gate, next); break;
+        case (2 << 4) | 2: tiled_group_record<2, 4, 2>(r, xs, lane, p, gate, next); break;
+        case (2 << 4) | 1: tiled_group_record<2, 4, 1>(r, xs, lane, p, gate, next); break;
+        case (4 << 4) | 2: tiled_group_record<4, 4, 2>(r, xs, lane, p, gate, next); break;
+        case (4 << 4) | 1: tiled_group_record<4, 4, 1>(r, xs, lane, p, gate, next); break;
+        case (8 << 4) | 1: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate, next); break;
+        default: tiled_wide_record<4>(r, g, xs, lane, p, gate, next); break;  // g = 16, 32
     }
 }
 
-// Persistent grid (1 or 2 CTAs per SM, kConsumerWarpsPerSm above), warp-specialised:
+// Persistent grid (1 or 2 CTAs per SM, kConsumerWarpsPerSm above), warp-specialised.
+// A launch covers one matrix or a group of independent products (TiledMember each):
+// CTA b works on member cta_work[b].x only -- its x, its static tile range, its tail
+// queue -- so a group pays one launch ramp and one tail for all of its matrices.
 //   * producer warp: streams this CTA's tiles HBM -> shared memory with cp.async.bulk
 //     into the stage pool, L2 evict_first: first its static tile range (the first tiles
 //     before griddepcontrol.wait -- the weights never depend on the previous kernel, so
-//     they stream under the predecessor's tail), then tiles from the launch's tail queue
+//     they stream under the predecessor's tail), then tiles from its member's tail queue
 //     until it is empty. The queue (the cheapest ~5 % of the work, most expensive
-//     first) goes to whichever CTAs run ahead, so the launch's CTAs finish together: the
-//     static split alone leaves a +-12 % spread of per-CTA times (HBM and SM variation a
-//     cost model cannot see), i.e. a ~3 us tail per launch;
+//     first) goes to whichever CTAs run ahead, so the CTAs finish together: the static
+//     split alone leaves a +-12 % spread of per-CTA times (HBM and SM variation a cost
+//     model cannot see), i.e. a ~3 us tail per launch;
 //   * consumer warps: wait for the predecessor (x producer) and for x in shared
 //     memory, then take records in issue order from a shared counter.
-// Overwrite without a memset launch (zero_y): every CTA zeroes its slice of y, then
-// bumps a 64-bit generation counter; warps pass the gate (counter reached the
-// generation's multiple of gridDim.x) before their first red.global. PDL dependents
-// are released only after the arrival, so back-to-back launches of one handle never
-// interleave their generations. The queue counter is reset by the launch's last CTA
-// once every CTA has drawn its last (failing) ticket; the next launch on the stream
-// draws only after its griddepcontrol.wait, i.e. after that reset.
+// Overwrite without a memset launch (zero_y): see YGate. A member's queue counter is
+// reset by its last CTA once every CTA of the member has drawn its last (failing)
+// ticket; the next launch on the stream draws only after its griddepcontrol.wait, i.e.
+// after that reset.
 template <bool kFull, int NC>
 __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     ecsr_tiled_kernel(const __grid_constant__ TiledParams p) {
     constexpr int kProducerWarp = NC;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + p.nstages;
-    uint64_t* xbar = empty + p.nstages;  // x staged (bulk copy or consumer copy)
-    uint8_t* stages = smem + ((16 * p.nstages + 8 + 127) & ~127);
-    __half* xs = reinterpret_cast<__half*>(stages + p.nstages * p.stage_bytes);
     __shared__ unsigned long long gate_target;
     __shared__ uint32_t gate_state;                 // 0 closed, 1 a warp polls, 2 open
     __shared__ uint32_t rec_next;                   // record claim counter
@@ -557,15 +635,21 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     // one 64-bit store / load, so a consumer never sees half an entry
     __shared__ unsigned long long tile_stage[32];
 
+    const uint4 work = p.cta_work[blockIdx.x];  // {member, [t0, t1) static tiles, slice}
+    const TiledMember& me = p.mem[work.x];
+    const uint32_t t0 = work.y, t1 = work.z;
+    const int nstages = me.nstages, stage_bytes = me.stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* xbar = full + nstages;  // x staged (bulk copy or consumer copy)
+    uint8_t* stages = smem + ((8 * nstages + 8 + 127) & ~127);
+    __half* xs = reinterpret_cast<__half*>(stages + nstages * stage_bytes);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t t0 = p.cta_tile[2 * blockIdx.x];  // [t0, t1): this CTA's static tiles
-    const uint32_t t1 = p.cta_tile[2 * blockIdx.x + 1];
     // x by one bulk copy when it is 16-B aligned and a multiple of 16 bytes
-    const bool x_bulk = p.x_vec16 && (p.K & 7) == 0 && p.K > 0;
+    const bool x_bulk = me.x_vec16 && (me.K & 7) == 0 && me.K > 0;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < p.nstages; ++s) {
+        for (int s = 0; s < nstages; ++s) {
             mbar_init(&full[s], 1);
             stage_done[s] = 0;
         }
@@ -602,7 +686,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             uint32_t freeset;
             while (true) {
                 uint32_t f = 0;
-                if (lane < p.nstages) {
+                if (lane < nstages) {
                     uint32_t done;
                     asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(done) : "r"(smem_addr(&stage_done[lane])) : "memory");
                     f = done == expect;
@@ -626,7 +710,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
                              "r"((li << 6) | (static_cast<uint32_t>(stage) << 1) | par), "r"(rec_end)
                              : "memory");
                 mbar_arrive_expect_tx(&full[stage], bytes);
-                bulk_g2s(stages + stage * p.stage_bytes, p.arena + static_cast<size_t>(a16) * 16u, bytes,
+                bulk_g2s(stages + stage * stage_bytes, me.arena + static_cast<size_t>(a16) * 16u, bytes,
                          &full[stage], policy);
             }
             fill_parity ^= 1u << stage;
@@ -635,11 +719,11 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         };
         // static tiles: their metadata rides in the lanes, 32 tiles per coalesced load
         uint32_t t = t0, win_base = t0;
-        uint2 win = t0 + lane < t1 ? p.tile_meta[t0 + lane] : make_uint2(0u, 0u);
+        uint2 win = t0 + lane < t1 ? me.tile_meta[t0 + lane] : make_uint2(0u, 0u);
         auto issue_static = [&]() {
             if (t - win_base >= 32u) {  // warp-uniform window slide
                 win_base = t;
-                win = t + lane < t1 ? p.tile_meta[t + lane] : make_uint2(0u, 0u);
+                win = t + lane < t1 ? me.tile_meta[t + lane] : make_uint2(0u, 0u);
             }
             const uint32_t a16 = __shfl_sync(0xffffffffu, win.x, t - win_base);
             const uint32_t info = __shfl_sync(0xffffffffu, win.y, t - win_base);
@@ -647,64 +731,59 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             ++t;
         };
         for (int k = 0; k < p.pre_tiles && t < t1; ++k) issue_static();
-        if (x_bulk || p.zero_y || p.nqueue) pdl_wait();
+        if (x_bulk || me.nqueue || p.zero_y) pdl_wait();
         if (x_bulk && lane == 0) {
-            const uint32_t xbytes = static_cast<uint32_t>(p.K) * 2u;
+            const uint32_t xbytes = static_cast<uint32_t>(me.K) * 2u;
             mbar_arrive_expect_tx(xbar, xbytes);
-            bulk_g2s(xs, p.x, xbytes, xbar, l2_evict_last_policy());
+            bulk_g2s(xs, me.x, xbytes, xbar, l2_evict_last_policy());
         }
         if (p.zero_y) {
-            // Overwrite mode without a memset launch: zero this CTA's slice of y (after
-            // the predecessor: y may alias its inputs), then bump the generation counter
-            // (release; covers the slice via the warp barrier) and publish the target in
-            // shared memory; PDL dependents are released only after the arrival. The
-            // atomic's latency overlaps the wait for x.
-            const int64_t r0 = p.M * blockIdx.x / gridDim.x, r1 = p.M * (blockIdx.x + 1) / gridDim.x;
-            for (int64_t r = r0 + lane; r < r1; r += 32) p.y[r] = 0.0f;
+            // Zero-y gate (after the predecessor: y may alias its inputs): zero this CTA's
+            // slice, count it (release), publish the target; PDL dependents are released
+            // only after the arrival, so launches on one workspace never mix generations.
+            zero_slice(p, work, lane, 32);
             __syncwarp();
             if (lane == 0) {
                 unsigned long long old;
-                asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.sync) : "memory");
-                const unsigned long long tgt = old - old % gridDim.x + gridDim.x;
-                asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_addr(&gate_target)), "l"(tgt + 1)
-                             : "memory");
+                asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.gate) : "memory");
+                atom_store_cta64(&gate_target, old - old % gridDim.x + gridDim.x + 1);
                 pdl_trigger();
             }
             __syncwarp();
         }
         mbar_wait(xbar, 0);
         while (t < t1) issue_static();
-        if (p.nqueue) {
+        if (me.nqueue) {
             // Tail queue: lanes 0..kTickets-1 each hold one drawn ticket and its tile's
             // metadata, so ticket and metadata latencies (~1 us each) overlap each other
             // and the wait for free stages; an exhausted lane stops drawing.
             uint32_t tk = 0xffffffffu;
             uint2 meta = make_uint2(0u, 0u);
             if (lane < kTickets) {
-                tk = atomicAdd(p.queue, 1u);
-                if (tk < p.nqueue) meta = p.tile_meta[p.queue_begin + tk];
+                tk = atomicAdd(me.queue, 1u);
+                if (tk < me.nqueue) meta = me.tile_meta[me.queue_begin + tk];
             }
             int head = 0;
             while (true) {
-                const uint32_t valid = __ballot_sync(0xffffffffu, tk < p.nqueue);
+                const uint32_t valid = __ballot_sync(0xffffffffu, tk < me.nqueue);
                 if (!valid) break;
                 // the next valid lane at or after head (round robin)
                 const uint32_t rot = (valid >> head) | (valid << ((32 - head) & 31));
                 const int src = (head + __ffs(rot) - 1) & 31;
                 issue_tile(__shfl_sync(0xffffffffu, meta.x, src), __shfl_sync(0xffffffffu, meta.y, src));
                 if (lane == src) {
-                    tk = atomicAdd(p.queue, 1u);
-                    if (tk < p.nqueue) meta = p.tile_meta[p.queue_begin + tk];
+                    tk = atomicAdd(me.queue, 1u);
+                    if (tk < me.nqueue) meta = me.tile_meta[me.queue_begin + tk];
                 }
                 head = (src + 1) % kTickets;
             }
             // every ticket this CTA drew has landed (its value was used): check out; the
-            // last CTA out resets the queue for the next launch on this workspace
+            // member's last CTA out resets its queue for the next launch on this workspace
             if (lane == 0) {
-                const uint32_t out = atomicAdd(p.queue + 1, 1u);
-                if (out == gridDim.x - 1) {
-                    p.queue[0] = 0u;
-                    p.queue[1] = 0u;
+                const uint32_t out = atomicAdd(me.queue + 1, 1u);
+                if (out == static_cast<uint32_t>(me.ctas) - 1u) {
+                    me.queue[0] = 0u;
+                    me.queue[1] = 0u;
                 }
             }
         }
@@ -720,11 +799,12 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
     pdl_wait();
     ECSR_TRACE(1, threadIdx.x == 0);
     if (!x_bulk) {
-        for (int i = tid; i < p.K; i += nthr) xs[i] = p.x[i];
+        for (int i = tid; i < me.K; i += nthr) xs[i] = me.x[i];
         consumer_bar_sync<NC>();
         if (tid == 0) mbar_arrive(xbar);
     }
-    YGate gate{p.sync, &gate_target, &gate_state, !p.zero_y};
+    const RecCtx rc{me.y, me.partials, &p};
+    YGate gate{&p, &gate_target, &gate_state, !p.zero_y};
     const uint32_t xs_addr = smem_addr(xs) + mbar_wait(xbar, 0);  // x gathers after x landed
     ECSR_TRACE(2, threadIdx.x == 0);
 
@@ -736,10 +816,25 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
 #ifdef ECSR_TRACE_CYCLES
     unsigned long long cyc_wait = 0, cyc_work = 0, nwork = 0, cyc_unissued = 0;
 #endif
+    // Each warp claims a record when it starts it. (ECSR_EXP_EARLY_CLAIM: claim the next
+    // one before the current one's lane reduction instead; measured slower, 1-4 %.)
+#ifdef ECSR_EXP_EARLY_CLAIM
+    uint32_t k_next = 0;
+    if (lane == 0) k_next = atomicAdd(&rec_next, 1u);
+    auto claim_next = [&]() {
+        if (lane == 0) k_next = atomicAdd(&rec_next, 1u);
+    };
+#else
+    auto claim_next = []() {};
+#endif
     while (true) {
+#ifdef ECSR_EXP_EARLY_CLAIM
+        const uint32_t k = __shfl_sync(0xffffffffu, k_next, 0);
+#else
         uint32_t k = 0;
         if (lane == 0) k = atomicAdd(&rec_next, 1u);
         k = __shfl_sync(0xffffffffu, k, 0);
+#endif
 #ifdef ECSR_TRACE_CYCLES
         const unsigned long long c0 = clock64();
 #endif
@@ -775,13 +870,13 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
         cyc_wait += c1 - c0;
 #endif
         ECSR_TRACE(3, threadIdx.x == 0 && ti == 0);
-        const uint32_t tile = stages_addr + stage * p.stage_bytes + tok;  // reads after the fill
+        const uint32_t tile = stages_addr + stage * stage_bytes + tok;  // reads after the fill
         uint32_t th[2];
         lds_bytes<8>(tile, th);
         const uint32_t gv = th[1] & 0xffffu;
         uint32_t off16;
         lds_bytes<2>(tile + 8 + 2 * (k - tile_begin), &off16);
-        tiled_record<kFull>(tile + 16u * (off16 & 0xffffu), gv, th[1] >> 16, xs_addr, lane, p, gate);
+        tiled_record<kFull>(tile + 16u * (off16 & 0xffffu), gv, th[1] >> 16, xs_addr, lane, rc, gate, claim_next);
 #ifdef ECSR_TRACE_CYCLES
         cyc_work += clock64() - c1;
         ++nwork;

@@ -183,12 +183,14 @@ def load_device(blob_or_path, device_dtype: str = "f16", force_generic: bool = F
 
 
 def spmv(W: DeviceMatrix, x, y=None, accumulate: bool = False, ordered: bool = False,
-         stream=None):
+         stream=None, memset_y: bool = False):
     """y = W x (y += W x with accumulate). x: device tensor [K] of W.x_dtype.
 
     ordered=True selects the bitwise-reproducible reduction (per-block partials summed
     per row in container order, exactly the reference's y order); the default uses
-    red.global.add.f32 and is the fast path.
+    red.global.add.f32 and is the fast path. memset_y makes the overwrite mode clear y
+    with a memset before an ungated launch (the path taken automatically when the whole
+    grid cannot be resident, e.g. under an MPS thread limit).
     """
     torch = _torch()
     if not isinstance(x, torch.Tensor) or not x.is_cuda:
@@ -209,13 +211,87 @@ def spmv(W: DeviceMatrix, x, y=None, accumulate: bool = False, ordered: bool = F
     elif not y.is_cuda or y.device.index != W.device_index:
         raise ValueError(f"y must be on cuda:{W.device_index}")
     mode = (_lib.SPMV_ACCUMULATE if accumulate else _lib.SPMV_OVERWRITE) | (
-        _lib.SPMV_ORDERED if ordered else 0)
+        _lib.SPMV_ORDERED if ordered else 0) | (_lib.SPMV_MEMSET_Y if memset_y else 0)
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
     rc = _lib.lib().ecsr_b200_spmv(W.handle, ctypes.c_void_p(x.data_ptr()),
                                    ctypes.c_void_p(y.data_ptr()), mode,
                                    ctypes.c_void_p(s.cuda_stream))
     _lib.check(rc, "ecsr_b200_spmv")
     return y
+
+
+class SpmvGroup:
+    """Several independent products y_i = W_i x_i in ONE launch (`ecsr_b200_group_*`).
+
+    The members' CTAs run side by side, so the group pays one launch ramp and one tail
+    instead of one per matrix -- e.g. the projections of a decoder layer whose inputs are
+    all ready. Every member must use the tiled layout; the group keeps references to its
+    matrices (they must outlive it)."""
+
+    def __init__(self, mats):
+        mats = list(mats)
+        if not mats:
+            raise ValueError("empty group")
+        if len({W.device_index for W in mats}) != 1:
+            raise ValueError("group members must be on one device")
+        self.mats = mats
+        self.device_index = mats[0].device_index
+        arr = (ctypes.c_void_p * len(mats))(*[W.handle.value for W in mats])
+        out = ctypes.c_void_p()
+        _lib.check(_lib.lib().ecsr_b200_group_create(arr, len(mats), ctypes.byref(out)),
+                   "ecsr_b200_group_create")
+        self._handle = out
+
+    def __len__(self):
+        return len(self.mats)
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h:
+            try:
+                _lib.lib().ecsr_b200_group_free(h)
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
+            self._handle = None
+
+    def info(self) -> dict:
+        launches, grid = ctypes.c_int32(), ctypes.c_int32()
+        ctas = (ctypes.c_int32 * len(self.mats))()
+        _lib.check(_lib.lib().ecsr_b200_group_info(self._handle, ctypes.byref(launches), ctypes.byref(grid),
+                                                   ctas, len(self.mats)), "ecsr_b200_group_info")
+        return {"launches": launches.value, "grid": grid.value, "ctas": list(ctas)}
+
+    def spmv(self, xs, ys=None, accumulate: bool = False, ordered: bool = False, stream=None,
+             memset_y: bool = False):
+        """ys[i] = W_i xs[i] (+= with accumulate) for every member, one launch."""
+        torch = _torch()
+        if len(xs) != len(self.mats):
+            raise ValueError(f"expected {len(self.mats)} inputs, got {len(xs)}")
+        if ys is None:
+            ys = [None] * len(self.mats)
+        outs = []
+        for W, x, y in zip(self.mats, xs, ys):
+            if not isinstance(x, torch.Tensor) or not x.is_cuda or x.shape != (W.num_cols,) \
+                    or x.dtype != W.x_dtype or x.device.index != W.device_index or not x.is_contiguous():
+                raise ValueError(f"each x must be a contiguous {W.x_dtype} CUDA tensor of shape ({W.num_cols},) "
+                                 f"on cuda:{W.device_index}")
+            if y is None:
+                y = torch.empty(W.num_rows, dtype=W.y_dtype, device=x.device)
+                if accumulate:
+                    y.zero_()
+            elif y.shape != (W.num_rows,) or y.dtype != W.y_dtype or not y.is_contiguous() \
+                    or not y.is_cuda or y.device.index != W.device_index:
+                raise ValueError(f"each y must be a contiguous {W.y_dtype} tensor of shape ({W.num_rows},) "
+                                 f"on cuda:{W.device_index}")
+            outs.append(y)
+        xa = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+        ya = (ctypes.c_void_p * len(outs))(*[y.data_ptr() for y in outs])
+        mode = (_lib.SPMV_ACCUMULATE if accumulate else _lib.SPMV_OVERWRITE) | (
+            _lib.SPMV_ORDERED if ordered else 0) | (_lib.SPMV_MEMSET_Y if memset_y else 0)
+        s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
+        _lib.check(_lib.lib().ecsr_b200_group_spmv(self._handle, xa, ya, mode, ctypes.c_void_p(s.cuda_stream)),
+                   "ecsr_b200_group_spmv")
+        return outs
 
 
 def spmv_host(W: DeviceMatrix, x: np.ndarray, ordered: bool = False) -> np.ndarray:

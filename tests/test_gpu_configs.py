@@ -1,4 +1,4 @@
-"""BASELINE.json configs 3-5 at full matrix sizes on the B200 (native encoder inputs).
+"""BASELINE.json configs 1-5 at full matrix sizes on the B200 (native encoder inputs).
 
 The reference encoder takes minutes to hours at these shapes, so the
 inputs come from the native encoder (byte-identical to the reference:
@@ -34,6 +34,17 @@ CASES = [
     ("OPT-30B-q 7168x7168 @70%", "magnitude", 7168, 7168, 0.7, 33, None),
     ("OPT-30B-fc2 7168x28672 @70%, shard 0/8", "magnitude", 7168, 28672, 0.7, 34, (0, 8)),
     ("70B-up 28672x8192 @50%, shard 5/8", "magnitude", 28672, 8192, 0.5, 35, (5, 8)),
+    # configs[0] and configs[1] at the sparsities the bench does not time
+    ("config-1 4096x4096 @50% seed 1", "magnitude", 4096, 4096, 0.5, 1, None),
+    ("7B-q 4096x4096 @60%", "magnitude", 4096, 4096, 0.6, 36, None),
+    ("7B-q 4096x4096 @70%", "magnitude", 4096, 4096, 0.7, 37, None),
+    ("7B-up 11008x4096 @60%", "magnitude", 11008, 4096, 0.6, 38, None),
+    ("7B-up 11008x4096 @70%", "magnitude", 11008, 4096, 0.7, 39, None),
+    ("7B-down 4096x11008 @60%", "magnitude", 4096, 11008, 0.6, 40, None),
+    ("7B-down 4096x11008 @70%", "magnitude", 4096, 11008, 0.7, 41, None),
+    ("OPT-30B-fc1 28672x7168 @70% unsharded", "magnitude", 28672, 7168, 0.7, 42, None),
+    # K > 65535: the u32-base record variant (ecsr_kernels.cuh, p.wide)
+    ("wide K 1024x70000 @90%", "magnitude", 1024, 70000, 0.9, 43, None),
 ]
 
 
@@ -77,3 +88,23 @@ def test_padding_is_multiplied_so_nonfinite_x_propagates():
     assert np.array_equal(np.isnan(y), np.isnan(ref)) and np.isnan(ref).any()
     fin = np.isfinite(ref)
     assert np.array_equal(y[fin], ref[fin])
+
+
+@pytest.mark.parametrize("shapes", [[(4096, 4096)] * 3, [(11008, 4096)] * 2],
+                         ids=["stacked q|k|v 3x4096x4096 @50%", "stacked gate|up 2x11008x4096 @50%"])
+def test_stacked_launch_parity(shapes):
+    # the bench's row-stacked launches (matrices sharing x packed as one handle)
+    from paper_2507_12205_b200.device import vstack
+
+    ecs = [convert_csr(make_matrix("magnitude", m, k, 0.5, 50 + i, dtype=np.float32))
+           for i, (m, k) in enumerate(shapes)]
+    ec = vstack(ecs)
+    W = to_device(ec)
+    assert W.layout == "tiled"
+    k = shapes[0][1]
+    x16 = np.random.default_rng(9).uniform(-1, 1, k).astype(np.float16)
+    ref16 = np.concatenate([oracle.spmv_ec_oracle(e.astype(np.float16).astype(np.float32),
+                                                  x16.astype(np.float32), np.float32) for e in ecs])
+    xd = torch.from_numpy(x16).cuda()
+    assert np.array_equal(spmv(W, xd, ordered=True).cpu().numpy(), ref16)
+    assert rel_err(spmv(W, xd).cpu().numpy(), ref16) <= 1e-5
