@@ -70,7 +70,15 @@ constexpr bool trace_caller_resets() { return false; }
 constexpr int kMaxStageBytes = 65536;   // largest tile a ring slot may hold
 constexpr int kMaxStages = 16;
 constexpr int kPackInternal = 1 << 30;  // spmv_set: unbounded u32 deltas (validated by range)
-constexpr double kQueueShare = 0.05;    // cost share of each CTA's range moved to the tail queue
+constexpr double kQueueShare = 0.05;       // cost share of each CTA's range drawn from the tail
+                                           // queue: a single matrix's launch
+constexpr double kGroupQueueShare = 0.30;  // the same for a grouped launch (one tail per step,
+                                           // members' CTAs sharing SMs: measured best 0.30)
+#ifdef ECSR_B200_TUNING
+double group_queue_share() { return env_int("ECSR_B200_GROUP_QPCT", 30) / 100.0; }
+#else
+double group_queue_share() { return kGroupQueueShare; }
+#endif
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
@@ -204,7 +212,10 @@ struct ecsr_dev {
     uint4* d_cta_work = nullptr;           // [grid] {member 0, tile lo, tile hi, slice} of each CTA
     double total_cost = 0;                 // summed tile cost (group CTA split)
     uint32_t* d_tile_meta = nullptr;       // [2 * ntiles] {start16, nrec | bytes16 << 16}
-    uint32_t queue_begin = 0, nqueue = 0;  // the launch's tail-queue tiles
+    uint32_t* d_queue_meta = nullptr;      // [2 * nqueue] the tail queue's tile metadata
+    uint32_t nqueue = 0;                   // tail-queue tiles of a launch of this handle alone
+    std::vector<uint32_t> tile_meta_h;     // host copy of d_tile_meta
+    std::vector<double> tile_cost_h;       // per tile (arena order): fitted consumer cost
     bool lean = false;                     // every run uses a lean-kernel record variant
     bool gate_ok = true;                   // the whole grid can be resident (zero-y gate)
     int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
@@ -616,6 +627,28 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
     tile_start16->push_back(static_cast<uint32_t>(arena->size() / 16));
 }
 
+// Tail queue of a launch: in every job's LPT-ordered static range [lo, hi) of handle d,
+// the cheapest suffix worth `share` of the range's cost moves to the queue (job.z
+// shrinks), drawn most expensive tile first by whichever CTAs of the member run ahead.
+// qmeta: the queue's {start16, info} pairs in draw order.
+void split_tail_queue(const ecsr_dev* d, std::vector<uint4>* jobs, double share, std::vector<uint32_t>* qmeta) {
+    std::vector<uint32_t> q;
+    for (uint4& j : *jobs) {
+        double rcost = 0, moved = 0;
+        for (uint32_t t = j.y; t < j.z; ++t) rcost += d->tile_cost_h[t];
+        uint32_t keep = j.z;
+        while (keep > j.y + 1 && moved + d->tile_cost_h[keep - 1] <= share * rcost) moved += d->tile_cost_h[--keep];
+        for (uint32_t t = keep; t < j.z; ++t) q.push_back(t);
+        j.z = keep;
+    }
+    std::stable_sort(q.begin(), q.end(), [&](uint32_t a, uint32_t b) { return d->tile_cost_h[a] > d->tile_cost_h[b]; });
+    qmeta->clear();
+    for (uint32_t t : q) {
+        qmeta->push_back(d->tile_meta_h[2 * t]);
+        qmeta->push_back(d->tile_meta_h[2 * t + 1]);
+    }
+}
+
 // Zero-y gate words of a launch (one counter on its own 128-B line).
 size_t gate_bytes(int) { return 8 * ecsr::kGateWords; }
 
@@ -806,6 +839,8 @@ struct MemberLaunch {
     void* partials;    // ordered mode
     int ctas;          // CTAs of the launch working on this member
     int nstages;       // stage-pool depth of its CTAs (the handle's, or a group's)
+    const uint32_t* queue_meta;  // the launch's tail queue of this member
+    uint32_t nqueue;
 };
 
 cudaError_t launch_tiled(const MemberLaunch* m, int n, const uint4* cta_work, int grid, int nc, bool lean,
@@ -823,8 +858,8 @@ cudaError_t launch_tiled(const MemberLaunch* m, int n, const uint4* cta_work, in
         t.partials = static_cast<float*>(m[i].partials);
         t.queue = m[i].queue;
         t.M = d->M;
-        t.queue_begin = d->queue_begin;
-        t.nqueue = d->nqueue;
+        t.queue_meta = reinterpret_cast<const uint2*>(m[i].queue_meta);
+        t.nqueue = m[i].nqueue;
         t.K = static_cast<int32_t>(d->K);
         t.stage_bytes = d->stage_bytes;
         t.nstages = m[i].nstages;
@@ -1038,7 +1073,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             // queue, most expensive tile first, drawn by whichever CTAs run ahead of the
             // cost model. Unpack identifies blocks by slot, not position.
             const double qshare = (flags & (0x80 << 16)) ? ((flags >> 16) & 0x7f) / 100.0 : kQueueShare;
-            std::vector<uint32_t> order, scta(grid + 1, 0), qtiles;
+            std::vector<uint32_t> order, scta(grid + 1, 0);
             order.reserve(ntiles);
             for (int c2 = 0; c2 < grid; ++c2) {
                 std::vector<uint32_t> ts;
@@ -1048,19 +1083,10 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                     const double cy = tcost[y] / std::max<uint32_t>(1, trec[y + 1] - trec[y]);
                     return cx > cy;
                 });
-                double rcost = 0, moved = 0;
-                for (uint32_t t : ts) rcost += tcost[t];
-                size_t keep = ts.size();
-                while (keep > 1 && moved + tcost[ts[keep - 1]] <= qshare * rcost) moved += tcost[ts[--keep]];
                 scta[c2] = static_cast<uint32_t>(order.size());
-                order.insert(order.end(), ts.begin(), ts.begin() + keep);
-                qtiles.insert(qtiles.end(), ts.begin() + keep, ts.end());
+                order.insert(order.end(), ts.begin(), ts.end());
             }
             scta[grid] = static_cast<uint32_t>(order.size());
-            std::stable_sort(qtiles.begin(), qtiles.end(), [&](uint32_t x, uint32_t y) { return tcost[x] > tcost[y]; });
-            d->queue_begin = static_cast<uint32_t>(order.size());
-            d->nqueue = static_cast<uint32_t>(qtiles.size());
-            order.insert(order.end(), qtiles.begin(), qtiles.end());
             {
                 std::vector<uint8_t> na;
                 na.reserve(arena.size());
@@ -1101,20 +1127,29 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                 if (d->d_tile_meta) d->allocs.push_back(d->d_tile_meta);
             }
             d->cta_tile_h = scta;
+            d->tile_meta_h = meta;
+            d->tile_cost_h = tcost;
             d->gate_ok = grid <= usable_sms(lim.sms) * ctas_per_sm;
             for (double c : tcost) d->total_cost += c;
+            std::vector<uint4> jobs(grid), work(grid);
+            for (int r = 0; r < grid; ++r) jobs[r] = make_uint4(0u, scta[r], scta[r + 1], static_cast<uint32_t>(r));
+            std::vector<uint32_t> qmeta;
+            split_tail_queue(d, &jobs, qshare, &qmeta);
+            d->nqueue = static_cast<uint32_t>(qmeta.size() / 2);
             std::vector<uint32_t> ranges(2 * grid);
-            std::vector<uint4> work(grid);
             for (int b = 0; b < grid; ++b) {
-                const int r = range_of_block(b, grid, ctas_per_sm);
-                ranges[2 * b] = scta[r];
-                ranges[2 * b + 1] = scta[r + 1];
-                work[b] = make_uint4(0u, scta[r], scta[r + 1], static_cast<uint32_t>(r));
+                work[b] = jobs[range_of_block(b, grid, ctas_per_sm)];
+                ranges[2 * b] = work[b].y;
+                ranges[2 * b + 1] = work[b].z;
             }
             d->cta_range_h = ranges;
             if (err == cudaSuccess) {
                 d->d_cta_work = dalloc_copy(work, &total, &err);
                 if (d->d_cta_work) d->allocs.push_back(d->d_cta_work);
+            }
+            if (err == cudaSuccess) {
+                d->d_queue_meta = dalloc_copy(qmeta, &total, &err);
+                if (d->d_queue_meta) d->allocs.push_back(d->d_queue_meta);
             }
             if (err != cudaSuccess) {
                 delete d;
@@ -1188,7 +1223,7 @@ int ecsr_b200_spmv(const ecsr_dev* d, const void* x, void* y, int32_t mode, void
         // else (or on request) a memset first and an ungated launch
         const bool memset_y = !ordered && !accumulate && (!d->gate_ok || (mode & ECSR_SPMV_MEMSET_Y));
         if (memset_y) ECSR_CUDA(cudaMemsetAsync(y, 0, 4 * d->M, st));
-        const MemberLaunch m{d, x, y, ws->queue, ws->partials, d->grid, d->nstages};
+        const MemberLaunch m{d, x, y, ws->queue, ws->partials, d->grid, d->nstages, d->d_queue_meta, d->nqueue};
         ECSR_CUDA(launch_tiled(&m, 1, d->d_cta_work, d->grid, ecsr::kConsumerWarpsPerSm / d->ctas_per_sm, d->lean,
                                d->smem_bytes, ws->gate, ordered, !ordered && !accumulate && !memset_y, trace, st));
         if (ordered) ECSR_CUDA(launch_finish<float>(d, y, accumulate, ws->partials, st));
@@ -1221,6 +1256,8 @@ struct ecsr_group {
         std::vector<int> idx;   // members of this launch (group order)
         std::vector<int> ctas;  // CTAs per member
         std::vector<int> nst;   // stage-pool depth per member in this launch
+        std::vector<uint32_t*> qmeta;  // per member: this launch's tail queue (device)
+        std::vector<uint32_t> nqueue;
         int grid = 0, nc = 8, smem = 0, cps = 2;
         bool lean = true, gate_ok = true;
         uint4* d_cta_work = nullptr;
@@ -1256,7 +1293,7 @@ namespace {
 // CTA merging its static ranges [j R / c, (j + 1) R / c) (contiguous in the arena, equal
 // cost each); co-resident CTAs pair one member's first ranges with another's last.
 int plan_part(const std::vector<const ecsr_dev*>& mats, const DeviceLimits& lim, ecsr_group::Part* pt,
-              std::vector<uint4>* work) {
+              std::vector<uint4>* work, std::vector<std::vector<uint32_t>>* qmetas) {
     const int n = static_cast<int>(pt->idx.size());
     pt->nc = ecsr::kConsumerWarpsPerSm / pt->cps;
     int64_t cap = 0;
@@ -1299,15 +1336,19 @@ int plan_part(const std::vector<const ecsr_dev*>& mats, const DeviceLimits& lim,
     pt->ctas = c;
     pt->gate_ok = pt->grid <= usable_sms(lim.sms) * pt->cps;
     std::vector<uint4> jobs;
+    qmetas->assign(n, {});
     for (int k = 0; k < n; ++k) {
         const ecsr_dev* d = mats[pt->idx[k]];
         const int R = d->grid;
+        std::vector<uint4> mj;
         for (int j = 0; j < c[k]; ++j) {
             const int r0 = static_cast<int>(static_cast<int64_t>(j) * R / c[k]);
             const int r1 = static_cast<int>(static_cast<int64_t>(j + 1) * R / c[k]);
-            jobs.push_back(make_uint4(static_cast<uint32_t>(k), d->cta_tile_h[r0], d->cta_tile_h[r1],
-                                      static_cast<uint32_t>(j)));
+            mj.push_back(make_uint4(static_cast<uint32_t>(k), d->cta_tile_h[r0], d->cta_tile_h[r1],
+                                    static_cast<uint32_t>(j)));
         }
+        split_tail_queue(d, &mj, group_queue_share(), &(*qmetas)[k]);
+        jobs.insert(jobs.end(), mj.begin(), mj.end());
     }
     work->assign(pt->grid, make_uint4(0, 0, 0, 0));
     for (int b = 0; b < pt->grid; ++b) (*work)[b] = jobs[range_of_block(b, pt->grid, pt->cps)];
@@ -1351,11 +1392,18 @@ int ecsr_b200_group_create(const ecsr_dev* const* mats, int32_t n, ecsr_group** 
     size_t off = 0;
     for (auto& pt : g->parts) {
         std::vector<uint4> work;
-        plan_part(g->mats, lim, &pt, &work);
+        std::vector<std::vector<uint32_t>> qmetas;
+        plan_part(g->mats, lim, &pt, &work, &qmetas);
         int64_t total_bytes = 0;
         cudaError_t err = cudaSuccess;
         pt.d_cta_work = dalloc_copy(work, &total_bytes, &err);
         if (pt.d_cta_work) g->allocs.push_back(pt.d_cta_work);
+        for (auto& q : qmetas) {
+            uint32_t* dq = err == cudaSuccess ? dalloc_copy(q, &total_bytes, &err) : nullptr;
+            if (dq) g->allocs.push_back(dq);
+            pt.qmeta.push_back(dq);
+            pt.nqueue.push_back(static_cast<uint32_t>(q.size() / 2));
+        }
         if (err == cudaSuccess) rc = configure_tiled_kernels(g->device, pt.smem);
         else rc = fail(ECSR_ERR_CUDA, std::string("group schedule: ") + cudaGetErrorString(err));
         if (rc) {
@@ -1404,7 +1452,7 @@ int ecsr_b200_group_spmv(const ecsr_group* g, const void* const* xs, void* const
         for (int j = 0; j < k; ++j) {
             const int i = pt.idx[j];
             m[j] = MemberLaunch{g->mats[i], xs[i], ys[i], reinterpret_cast<uint32_t*>(ws + g->queue_off + 128 * i),
-                                nullptr, pt.ctas[j], pt.nst[j]};
+                                nullptr, pt.ctas[j], pt.nst[j], pt.qmeta[j], pt.nqueue[j]};
         }
         const bool overwrite = (mode & ECSR_SPMV_ACCUMULATE) == 0;
         const bool memset_y = overwrite && (!pt.gate_ok || (mode & ECSR_SPMV_MEMSET_Y));

@@ -53,7 +53,7 @@ struct TiledMember {
     float* partials;               // [nslots] (ordered mode)
     uint32_t* queue;               // [2] tail queue {next tile, CTAs done} (per-stream workspace)
     int64_t M;
-    uint32_t queue_begin;          // tiles [queue_begin, queue_begin + nqueue) go through the queue
+    const uint2* queue_meta;       // [nqueue] the launch's tail queue (tile metadata, draw order)
     uint32_t nqueue;
     int32_t K;
     int32_t stage_bytes;
@@ -761,7 +761,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             uint2 meta = make_uint2(0u, 0u);
             if (lane < kTickets) {
                 tk = atomicAdd(me.queue, 1u);
-                if (tk < me.nqueue) meta = me.tile_meta[me.queue_begin + tk];
+                if (tk < me.nqueue) meta = me.queue_meta[tk];
             }
             int head = 0;
             while (true) {
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
                 issue_tile(__shfl_sync(0xffffffffu, meta.x, src), __shfl_sync(0xffffffffu, meta.y, src));
                 if (lane == src) {
                     tk = atomicAdd(me.queue, 1u);
-                    if (tk < me.nqueue) meta = me.tile_meta[me.queue_begin + tk];
+                    if (tk < me.nqueue) meta = me.queue_meta[tk];
                 }
                 head = (src + 1) % kTickets;
             }

@@ -1,5 +1,5 @@
-"""Sweep the grouped step over packing / launch knobs (tuning build): tile size,
-tail-queue share, tiles streamed before griddepcontrol.wait. Encodes once.
+"""Sweep the tail-queue share of the grouped step (ECSR_B200_GROUP_QPCT) and of the
+chained step (the handles' pack-time share), tuning build. Encodes once.
 
     python scripts/group_sweep.py build/libNAME.so [workload]"""
 import os
@@ -25,12 +25,12 @@ xs = [torch.randn(stacked[ln].num_cols, device="cuda").half() for ln, _ in launc
 ys = [torch.empty(stacked[ln].num_rows, device="cuda") for ln, _ in launches]
 
 
-def run(tile_kb=None, queue_pct=None, pre=None, chained=False):
-    if pre is None:
-        os.environ.pop("ECSR_B200_PRE", None)
+def run(queue_pct=None, chained=False):
+    if chained:
+        Ws = [to_device(stacked[ln], queue_pct=queue_pct) for ln, _ in launches]
     else:
-        os.environ["ECSR_B200_PRE"] = str(pre)
-    Ws = [to_device(stacked[ln], tile_kb=tile_kb, queue_pct=queue_pct) for ln, _ in launches]
+        os.environ["ECSR_B200_GROUP_QPCT"] = str(queue_pct)
+        Ws = [to_device(stacked[ln]) for ln, _ in launches]
     g = SpmvGroup(Ws)
 
     def body():
@@ -50,12 +50,12 @@ def run(tile_kb=None, queue_pct=None, pre=None, chained=False):
             body()
     ms, _ = bench.time_graph(gr, 20, 3, stream)
     ms /= 5
-    print(f"{name} {'chained' if chained else 'grouped'} tile_kb={tile_kb} queue_pct={queue_pct} pre={pre}: "
+    print(f"{name} {'chained, handle' if chained else 'grouped, group'} queue_pct={queue_pct}: "
           f"{ms * 1e3:.2f} us {step_bytes / (ms * 1e-3) / 1e9:.0f} GB/s", flush=True)
     del g, Ws
 
 
-qs = [int(v) for v in os.environ.get("QS", "5,30,40,50,60,75,90,100").split(",")]
-for chained in (False, True):
-    for q in qs:
-        run(queue_pct=q, chained=chained)
+for q in [int(v) for v in os.environ.get("QG", "20,25,30,35").split(",")]:
+    run(queue_pct=q)
+for q in [int(v) for v in os.environ.get("QC", "5,15,30").split(",")]:
+    run(queue_pct=q, chained=True)

@@ -5,8 +5,8 @@ tiled kernel: small containers, every launch mode, checked against the oracle.
 
 Covers: the smoke container (one tile per CTA), a 1024x4096 matrix packed with 1 KB
 tiles (many tiles per CTA: the stage pool, the tile->stage map and the tail queue
-wrap), the u32-base (K > 65535) variant, two streams sharing one handle, and
-overwrite / accumulate / ordered modes."""
+wrap), the u32-base (K > 65535) variant, two streams sharing one handle, overwrite /
+accumulate / ordered modes, and a grouped launch (gated and memset overwrite)."""
 import os
 import sys
 
@@ -63,4 +63,19 @@ print("tiles", W.bytes()["tiles"], "grid", W.bytes()["grid"], "queue", W.bytes()
 check(ec, W, np.random.default_rng(1).uniform(-1, 1, 4096), "1024x4096 1 KB tiles")
 ec = convert_csr(make_matrix("magnitude", 256, 70000, 0.995, 9, dtype=np.float32))
 check(ec, to_device(ec), np.random.default_rng(2).uniform(-1, 1, 70000), "256x70000 wide bases")
+# a grouped launch of three matrices (x of 8 KB and 22 KB side by side), gated and memset
+from paper_2507_12205_b200.device import SpmvGroup  # noqa: E402
+
+ecs = [convert_csr(make_matrix("magnitude", m, k, 0.5, 11 + i, dtype=np.float32))
+       for i, (m, k) in enumerate([(512, 4096), (256, 4096), (256, 11008)])]
+g = SpmvGroup([to_device(e) for e in ecs])
+xs = [np.random.default_rng(3 + i).uniform(-1, 1, e.num_cols) for i, e in enumerate(ecs)]
+xd = [torch.from_numpy(x.astype(np.float16)).cuda() for x in xs]
+for memset_y in (False, True, False):
+    ys = g.spmv(xd, memset_y=memset_y)
+    for e, x, y in zip(ecs, xs, ys):
+        r = ref16(e, x)
+        err = np.max(np.abs(y.cpu().numpy() - r)) / max(np.max(np.abs(r)), 1e-30)
+        assert err <= 1e-5, ("group", err)
+print("group of 3: ok", flush=True)
 print("sanitize workload done")
