@@ -833,9 +833,10 @@ def load_shards(rank, world):
 
 
 def run_sharded(args):
-    """N > 1: every matrix row-sharded over the ranks (byte-balanced, shard-first),
-    x replicated; one coalesced NCCL all-gather per step assembles every launch's y
-    straight into its final layout (strong scaling)."""
+    """N > 1: every matrix row-sharded over the ranks (byte-balanced, shard-first), x
+    replicated; one grouped SpMV launch per rank and one exchange per step assemble every
+    launch's y in its final layout on every rank -- by default the peer-memory exchange
+    kernel (ecsr_b200_xchg_run), or NCCL all-gather + index assembly (strong scaling)."""
     import torch
     import torch.distributed as dist
 
@@ -887,8 +888,20 @@ def run_sharded(args):
                 idx.append(r * o + offs[ln] + within + np.arange(b[r + 1] - b[r]))
         gidx[ln] = torch.from_numpy(np.concatenate(idx)).to(dev)
     yfull = {ln: torch.empty(int(gidx[ln].numel()), dtype=torch.float32, device=dev) for ln, _ in launches}
-    yfull_host = {ln: torch.empty(yfull[ln].shape, dtype=torch.float32).pin_memory() for ln in yfull}
     stream = torch.cuda.Stream(dev)
+    peer = None
+    if args.exchange == "peer":
+        # the y exchange over NVLink peer memory: one kernel PDL-chained behind the
+        # grouped SpMV stores this rank's rows into every rank's y_full (final layout)
+        from paper_2507_12205_b200.exchange import PeerExchange, shard_segments
+
+        rows = [int(gidx[ln].numel()) for ln, _ in launches]
+        y_off = np.concatenate([[0], np.cumsum(rows)[:-1]]).astype(int).tolist()
+        peer = PeerExchange(sum(rows), rank, world)
+        peer.plan(shard_segments([plans[ln].bounds for ln, _ in launches], [offs[ln] for ln, _ in launches],
+                                 y_off, rank))
+        yfull = {ln: peer.y[o:o + n] for (ln, _), o, n in zip(launches, y_off, rows)}
+    yfull_host = {ln: torch.empty(yfull[ln].shape, dtype=torch.float32).pin_memory() for ln in yfull}
 
     from paper_2507_12205_b200.device import SpmvGroup
 
@@ -900,6 +913,9 @@ def run_sharded(args):
         group.spmv(x_list, y_list, stream=stream)
 
     def exchange():
+        if peer is not None:
+            peer.run(send, stream)
+            return
         dist.all_gather_into_tensor(recv, send)
         for ln, _ in launches:
             torch.index_select(recv, 0, gidx[ln], out=yfull[ln])
@@ -984,7 +1000,8 @@ def run_sharded(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16 values/x, f32 accumulate", "data": "synthetic",
-            "config": cfg, "parallelism": f"row-shard{world}+nccl-allgather",
+            "config": cfg,
+            "parallelism": f"row-shard{world}+" + ("peer-exchange" if peer is not None else "nccl-allgather"),
             "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -996,7 +1013,7 @@ def run_sharded(args):
             "clocks": clocks.summary(),
             "sharded": {"spmv_ms_per_step": round(spmv_ms, 5), "exchange_ms_per_step": round(gather_ms, 5),
                         "step_ms": round(ms, 5), "allgather_bytes_per_rank_per_step": int(send.numel()) * 4,
-                        "collectives_per_step": 1, "y_assembled_in_step": True},
+                        "exchange": args.exchange, "exchanges_per_step": 1, "y_assembled_in_step": True},
         }
         sys.stdout.flush()
         os.write(json_fd, (json.dumps(line) + "\n").encode())
@@ -1013,6 +1030,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--shard", action="store_true", help="use the row-sharded path even at N=1")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="sharded y exchange: NVLink peer stores (one kernel) or NCCL all-gather")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

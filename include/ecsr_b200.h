@@ -151,6 +151,29 @@ int ecsr_b200_group_spmv(const ecsr_group* group, const void* const* xs, void* c
 int ecsr_b200_group_info(const ecsr_group* group, int32_t* launches, int32_t* grid, int32_t* ctas,
                          int32_t k);
 void ecsr_b200_group_free(ecsr_group* group);
+/* Row-sharded y exchange over NVLink peer memory: every
+ * rank owns a y_full buffer (all ranks' rows in their final layout) that its peers map
+ * through CUDA IPC. ecsr_b200_xchg_run launches ONE kernel (PDL-chained behind the
+ * rank's shard SpMV) that stores this rank's segments of its SpMV output into every
+ * rank's y_full, signals each peer (system-scope release on a per-source flag) and
+ * waits until every peer's push into this rank landed -- the NCCL all-gather + index
+ * assembly of the sharded step in one launch. Setup: create (y_full bytes, rank,
+ * world <= 16), export handle (64 B) -> all-gather the handles (host) -> open, plan the
+ * segments once (src/dst byte offsets, multiples of 4). ecsr_b200_xchg_y: the local
+ * y_full. Steps are counted on the device, so the run can be graph-captured. */
+typedef struct ecsr_xchg ecsr_xchg;
+typedef struct ecsr_xchg_seg {
+    int64_t src_off;  /* bytes into the SpMV output passed to ecsr_b200_xchg_run */
+    int64_t dst_off;  /* bytes into every rank's y_full */
+    int64_t bytes;
+} ecsr_xchg_seg;
+int ecsr_b200_xchg_create(int64_t y_full_bytes, int32_t rank, int32_t world, ecsr_xchg** out);
+int ecsr_b200_xchg_handle(const ecsr_xchg* xchg, void* handle64);
+int ecsr_b200_xchg_open(ecsr_xchg* xchg, const void* handles /* world x 64 B */);
+int ecsr_b200_xchg_plan(ecsr_xchg* xchg, const ecsr_xchg_seg* segs, int32_t nsegs);
+int ecsr_b200_xchg_run(const ecsr_xchg* xchg, const void* src, void* stream);
+void* ecsr_b200_xchg_y(const ecsr_xchg* xchg);
+void ecsr_b200_xchg_free(ecsr_xchg* xchg);
 /* .ecsr wire format (storage.py:389-483) straight to a device handle, no numpy round trip
  * (SURVEY.md §8(f) #3). ecsr_b200_parse parses and shape-checks a blob on the host only,
  * rejecting corruption with the reference's ContainerError (code 1) and message: bad

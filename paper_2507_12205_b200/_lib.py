@@ -85,6 +85,13 @@ SIGNATURES = {
     "ecsr_b200_group_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
                                      ctypes.POINTER(c_i32), c_i32]),
     "ecsr_b200_group_free": (None, [c_vp]),
+    "ecsr_b200_xchg_create": (c_i32, [c_i64, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "ecsr_b200_xchg_handle": (c_i32, [c_vp, c_vp]),
+    "ecsr_b200_xchg_open": (c_i32, [c_vp, c_vp]),
+    "ecsr_b200_xchg_plan": (c_i32, [c_vp, c_vp, c_i32]),
+    "ecsr_b200_xchg_run": (c_i32, [c_vp, c_vp, c_vp]),
+    "ecsr_b200_xchg_y": (c_vp, [c_vp]),
+    "ecsr_b200_xchg_free": (None, [c_vp]),
     "ecsr_b200_trace": (c_i32, [c_vp, c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "ecsr_b200_spmv_set": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_i64, c_i32]),

@@ -42,6 +42,15 @@ constexpr int kConsumerWarpsPerSm = 16;
 __host__ __device__ constexpr int tiled_threads(int nc) { return 32 * (nc + 1); }
 constexpr int kMaxRingStages = 16;
 constexpr int kTickets = 3;     // tail-queue tickets a producer keeps in flight
+// Back-off of the producer's stage-pool poll and of a consumer waiting for its record's
+// tile to be issued (tuning builds may override them).
+#ifndef ECSR_PRODUCER_POLL_NS
+#define ECSR_PRODUCER_POLL_NS 20
+#endif
+#ifndef ECSR_CONSUMER_POLL_NS
+#define ECSR_CONSUMER_POLL_NS 64
+#endif
+constexpr unsigned kProducerPollNs = ECSR_PRODUCER_POLL_NS, kConsumerPollNs = ECSR_CONSUMER_POLL_NS;
 constexpr int kMaxMembers = 8;  // matrices of one grouped launch
 
 // One matrix of a (grouped) launch: its packed arena and this launch's x and y.
@@ -693,7 +702,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
                 }
                 freeset = __ballot_sync(0xffffffffu, f != 0);
                 if (freeset) break;
-                __nanosleep(20);
+                __nanosleep(kProducerPollNs);
             }
             const int stage = __ffs(freeset) - 1;
             const uint32_t nrec = info & 0xffffu;
@@ -858,7 +867,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             uint32_t fin;  // not issued (yet): past the CTA's last record?
             asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(fin) : "r"(smem_addr(&final_rec)) : "memory");
             if (k >= fin) break;
-            __nanosleep(64);
+            __nanosleep(kConsumerPollNs);
         }
         if (!have) break;
 #ifdef ECSR_TRACE_CYCLES
