@@ -781,13 +781,14 @@ int configure_tiled_kernels(int device, int smem) {
     std::lock_guard<std::mutex> lock(mu);
     if (device >= static_cast<int>(configured.size())) configured.resize(device + 1, 0);
     if (configured[device] >= smem) return ECSR_OK;
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, 8>,
+    constexpr int kHalf = ecsr::kConsumerWarpsPerSm / 2, kAll = ecsr::kConsumerWarpsPerSm;
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, kHalf>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, 8>,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, kHalf>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, 16>,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<true, kAll>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, 16>,
+    ECSR_CUDA(cudaFuncSetAttribute(ecsr::ecsr_tiled_kernel<false, kAll>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured[device] = smem;
     return ECSR_OK;
@@ -877,11 +878,12 @@ cudaError_t launch_tiled(const MemberLaunch* m, int n, const uint4* cta_work, in
     p.trace = trace;
     const bool coop = coop_launch();
     const dim3 blk(ecsr::tiled_threads(nc)), grd(grid);
-    if (nc == 8)
-        return lean ? launch_ex(ecsr::ecsr_tiled_kernel<false, 8>, grd, blk, smem, st, coop, p)
-                    : launch_ex(ecsr::ecsr_tiled_kernel<true, 8>, grd, blk, smem, st, coop, p);
-    return lean ? launch_ex(ecsr::ecsr_tiled_kernel<false, 16>, grd, blk, smem, st, coop, p)
-                : launch_ex(ecsr::ecsr_tiled_kernel<true, 16>, grd, blk, smem, st, coop, p);
+    constexpr int kHalf = ecsr::kConsumerWarpsPerSm / 2, kAll = ecsr::kConsumerWarpsPerSm;
+    if (nc == kHalf)
+        return lean ? launch_ex(ecsr::ecsr_tiled_kernel<false, kHalf>, grd, blk, smem, st, coop, p)
+                    : launch_ex(ecsr::ecsr_tiled_kernel<true, kHalf>, grd, blk, smem, st, coop, p);
+    return lean ? launch_ex(ecsr::ecsr_tiled_kernel<false, kAll>, grd, blk, smem, st, coop, p)
+                : launch_ex(ecsr::ecsr_tiled_kernel<true, kAll>, grd, blk, smem, st, coop, p);
 }
 
 template <typename T, typename VT, typename XT>
@@ -1269,6 +1271,7 @@ struct ecsr_group {
     size_t queue_off = 0, ws_bytes = 0;  // member i's queue: queue_off + 128 * i
     static constexpr int kStreamSlots = 4;
     uint8_t* ws_base = nullptr;          // kStreamSlots workspaces of ws_bytes
+    unsigned long long* d_trace = nullptr;  // tuning builds: per-CTA timeline of part 0
     mutable cudaStream_t ws_stream[kStreamSlots] = {};
     mutable int ws_bound = 0;
     mutable std::mutex ws_mu;
@@ -1458,9 +1461,19 @@ int ecsr_b200_group_spmv(const ecsr_group* g, const void* const* xs, void* const
         const bool memset_y = overwrite && (!pt.gate_ok || (mode & ECSR_SPMV_MEMSET_Y));
         if (memset_y)
             for (int j = 0; j < k; ++j) ECSR_CUDA(cudaMemsetAsync(m[j].y, 0, 4 * m[j].d->M, st));
+        unsigned long long* trace = nullptr;
+        if (trace_enabled() && &pt == &g->parts[0]) {  // tuning builds only (caller resets)
+            ecsr_group* gm = const_cast<ecsr_group*>(g);
+            if (!gm->d_trace) {
+                ECSR_CUDA(cudaMalloc(&gm->d_trace, 8 * 16 * pt.grid));
+                ECSR_CUDA(cudaMemset(gm->d_trace, 0, 8 * 16 * pt.grid));
+                gm->allocs.push_back(gm->d_trace);
+            }
+            trace = gm->d_trace;
+        }
         ECSR_CUDA(launch_tiled(m, k, pt.d_cta_work, pt.grid, pt.nc, pt.lean, pt.smem,
                                reinterpret_cast<unsigned long long*>(ws + pt.gate_off), false,
-                               overwrite && !memset_y, nullptr, st));
+                               overwrite && !memset_y, trace, st));
     }
     return ECSR_OK;
 }
@@ -1478,6 +1491,22 @@ int ecsr_b200_group_info(const ecsr_group* g, int32_t* launches, int32_t* grid, 
 }
 
 void ecsr_b200_group_free(ecsr_group* g) { delete g; }
+
+// Internal tuning aid: the per-CTA timeline of a group's first launch (16 u64 per CTA;
+// reset = zero it, with slot 7 = ~0).
+int ecsr_b200_debug_group_trace(ecsr_group* g, unsigned long long* out, int64_t n, int32_t reset) {
+    if (!g || g->parts.empty()) return fail(ECSR_ERR_VALUE, "no group");
+    const int grid = g->parts[0].grid;
+    if (!g->d_trace) return fail(ECSR_ERR_VALUE, "no trace recorded");
+    if (reset) {
+        std::vector<unsigned long long> init(16 * grid, 0ull);
+        for (int c = 0; c < grid; ++c) init[16 * c + 7] = ~0ull;
+        ECSR_CUDA(cudaMemcpy(g->d_trace, init.data(), 8 * init.size(), cudaMemcpyHostToDevice));
+        return ECSR_OK;
+    }
+    ECSR_CUDA(cudaMemcpy(out, g->d_trace, 8 * std::min<int64_t>(n, 16 * grid), cudaMemcpyDeviceToHost));
+    return ECSR_OK;
+}
 
 int ecsr_b200_info(const ecsr_dev* d, int64_t* num_rows, int64_t* num_cols, int32_t* nsets,
                    int32_t* warp_size, int32_t* delta_bits, int32_t* value_bits, int32_t* device_dtype) {

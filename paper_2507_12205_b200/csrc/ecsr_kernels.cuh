@@ -38,7 +38,10 @@ namespace ecsr {
 
 // 16 consumer warps per SM: either 2 co-resident CTAs of 8 (consecutive launches
 // overlap; x fits twice) or 1 CTA of 16 (large K: x would not leave room for stages).
-constexpr int kConsumerWarpsPerSm = 16;
+#ifndef ECSR_CONSUMER_WARPS_PER_SM
+#define ECSR_CONSUMER_WARPS_PER_SM 16
+#endif
+constexpr int kConsumerWarpsPerSm = ECSR_CONSUMER_WARPS_PER_SM;
 __host__ __device__ constexpr int tiled_threads(int nc) { return 32 * (nc + 1); }
 constexpr int kMaxRingStages = 16;
 constexpr int kTickets = 3;     // tail-queue tickets a producer keeps in flight

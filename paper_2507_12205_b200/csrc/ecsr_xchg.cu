@@ -73,24 +73,31 @@ __global__ void __launch_bounds__(256) ecsr_xchg_kernel(const __grid_constant__ 
                 reinterpret_cast<uint32_t*>(b)[i] = reinterpret_cast<const uint32_t*>(a)[i];
         }
     }
-#ifndef ECSR_XCHG_CTA_FENCE
-    __threadfence_system();  // this thread's stores are visible system-wide ...
-    __syncthreads();         // ... for every thread of the CTA, before the signal
-#else
+    // every thread's stores, then one system-scope fence for the CTA (the pattern of
+    // cooperative groups' grid sync: bar.sync, then thread 0 fences and signals)
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
-#endif
     if (threadIdx.x == 0) {
         unsigned long long* flag =
             reinterpret_cast<unsigned long long*>(dst + p.flags_off + static_cast<int64_t>(p.rank) * kLine);
+#ifdef ECSR_XCHG_GPU_SCOPE
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(flag) : "memory");
+#else
         asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(flag) : "memory");
+#endif
         // wait for rank q's push into this rank (its flag slot in our own buffer)
         const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(
             p.peer_base[p.rank] + p.flags_off + static_cast<int64_t>(q) * kLine);
         unsigned long long v;
+#ifndef ECSR_XCHG_NO_WAIT
         do {
+#ifdef ECSR_XCHG_GPU_SCOPE
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+#else
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+#endif
         } while (v < step * static_cast<unsigned long long>(p.parts));  // all of rank q's slices
+#endif
         // the last CTA of the exchange advances the step (the next exchange on this
         // stream reads it after its griddepcontrol.wait, i.e. after this grid completed)
         if (atomicAdd(p.done_word, 1u) == gridDim.x - 1u) {

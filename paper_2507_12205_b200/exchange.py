@@ -57,16 +57,26 @@ class PeerExchange:
         self.rank, self.world, self.n = int(rank), int(world), int(y_full_floats)
         lib = _lib.lib()
         h = ctypes.c_void_p()
-        _lib.check(lib.ecsr_b200_xchg_create(4 * self.n, self.rank, self.world, ctypes.byref(h)),
-                   "ecsr_b200_xchg_create")
         self._h = h
-        mine = (ctypes.c_uint8 * 64)()
-        _lib.check(lib.ecsr_b200_xchg_handle(h, mine), "ecsr_b200_xchg_handle")
+        mine, err = None, None
+        try:  # a failing rank still takes part in the handle all-gather below
+            _lib.check(lib.ecsr_b200_xchg_create(4 * self.n, self.rank, self.world, ctypes.byref(h)),
+                       "ecsr_b200_xchg_create")
+            self._h = h
+            buf = (ctypes.c_uint8 * 64)()
+            _lib.check(lib.ecsr_b200_xchg_handle(h, buf), "ecsr_b200_xchg_handle")
+            mine = bytes(buf)
+        except Exception as exc:  # noqa: BLE001
+            err = exc
         if self.world > 1:
             handles = [None] * self.world
-            dist.all_gather_object(handles, bytes(mine), group=group)
+            dist.all_gather_object(handles, mine, group=group)
         else:
-            handles = [bytes(mine)]
+            handles = [mine]
+        if err is not None:
+            raise err
+        if any(x is None for x in handles):
+            raise RuntimeError("peer exchange: another rank could not create its buffer")
         allh = (ctypes.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(handles))
         _lib.check(lib.ecsr_b200_xchg_open(h, allh), "ecsr_b200_xchg_open")
         ptr = lib.ecsr_b200_xchg_y(h)

@@ -14,8 +14,8 @@ from paper_2507_12205_b200.exchange import PeerExchange  # noqa: E402
 
 rows = [12288, 4096, 22016, 4096]
 segs, o = [], 0
-for r in rows:  # one matrix set per launch, unaligned-ish offsets like real shards
-    segs.append((o + 1, o + 1, r - 1))
+for r in rows:  # one matrix set per launch, offsets not 16-B aligned like real shards
+    segs.append((o + 1, o + 1, r))
     o += r
 src = torch.randn(o + 8, device="cuda")
 ex = PeerExchange(o + 8, 0, 1)
@@ -25,7 +25,7 @@ with torch.cuda.stream(s):
     for _ in range(3):
         ex.run(src, s)
 torch.cuda.synchronize()
-assert torch.equal(ex.y[1:o], src[1:o])
+assert torch.equal(ex.y[1:o + 1], src[1:o + 1])
 for n in (1, 20):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
