@@ -218,7 +218,7 @@ struct ecsr_dev {
     std::vector<double> tile_cost_h;       // per tile (arena order): fitted consumer cost
     bool lean = false;                     // every run uses a lean-kernel record variant
     bool gate_ok = true;                   // the whole grid can be resident (zero-y gate)
-    int ctas_per_sm = 2;                   // co-resident CTAs per SM (8 or 16 consumer warps)
+    int ctas_per_sm = 2;                   // co-resident CTAs per SM (9 or 18 consumer warps)
     std::vector<TileFeat> tile_feat;       // per tile (cost-model calibration)
     std::vector<uint32_t> cta_tile_h;      // host copy of the CTA tile boundaries
     std::vector<uint32_t> cta_range_h;     // per block [lo, hi) (launch order)
@@ -1013,8 +1013,8 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
             if ((sets[si].block_indptr[b + 1] - sets[si].block_indptr[b]) / (32 * v) > 65535) tiled = false;
     }
     const bool wide = num_cols > 65535;
-    // Two co-resident CTAs per SM (8 consumer warps each; consecutive launches overlap)
-    // while x is small; one CTA of 16 consumer warps when two copies of x would crowd
+    // Two co-resident CTAs per SM (9 consumer warps each; consecutive launches overlap)
+    // while x is small; one CTA of 18 consumer warps when two copies of x would crowd
     // out the stage pool.
     const int64_t xbytes = round_up(2 * std::max<int64_t>(num_cols, 1), 16);
     const int ctas_per_sm = xbytes <= 32768 ? 2 : 1;

@@ -13,6 +13,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
+from paper_2507_12205_b200 import _lib  # noqa: E402
+
+if len(sys.argv) > 1:  # a tuning build (scripts/build_exp.sh) instead of the product library
+    _lib.LIB_PATH = os.path.abspath(sys.argv[1])
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
