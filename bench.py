@@ -37,10 +37,12 @@ Reported (one JSON line, rank 0):
                bounded sample of the same workload.
 
 `--impl reference` runs the UNMODIFIED reference package (baseline/_ref: `ecsr`, its
-compiled backend) on the same workload: encodes with the reference's convert_csr
-(parallel processes, one matrix each, cached in cache/), then times the stock
-single-process `executor.spmv_ec(ec, x, validate=False)` (executor.py:80-96) over the
-layer. libecsr_b200.so is never loaded on that path (checked from /proc/self/maps).
+compiled backend) on the same workload: its inputs are the same encodings, made before
+timing in a separate process (the native encoder by default, the reference's own
+convert_csr with --ref-inputs reference) and sha256-checked against the reference
+encodings; it then times the stock single-process `executor.spmv_ec(ec, x,
+validate=False)` (executor.py:80-96) over the layer. libecsr_b200.so is never loaded on
+that path (checked from /proc/self/maps).
 """
 
 from __future__ import annotations
@@ -309,19 +311,34 @@ def run_reference(args):
     backend = _kernels.active_backend()
     wl = WORKLOADS[HEADLINE]
     hashes = ref_hashes()
-    # 1. encodings: the reference pipeline, one process per missing matrix
+    # 1. encodings (setup, untimed). Missing blobs come from the reference's own
+    #    convert_csr (--ref-inputs reference: one process per matrix, ~3 min for the
+    #    11008-row ones) or, by default, from the native encoder run in a SEPARATE process
+    #    (this process never loads libecsr_b200.so). Either way every blob must be
+    #    sha256-equal to the pinned reference encoding (tests/golden/ref_hashes.json, made
+    #    with the reference's convert_csr) before it is timed.
     todo = [m for m in wl["matrices"] if not os.path.exists(cache_path(m))]
     enc_s = {}
-    if todo:
+    encoder = "reference storage.convert_csr (baseline/_ref)"
+    if todo and args.ref_inputs == "native":
+        t0 = time.perf_counter()
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--encode-cache"], check=True)
+        enc_s = {"native_subprocess_s": round(time.perf_counter() - t0, 1)}
+        encoder = "native encoder in a separate process, sha256-equal to reference convert_csr"
+    elif todo:
         with mp.get_context("spawn").Pool(min(len(todo), os.cpu_count() or 1)) as pool:
             for m, dt in zip(todo, pool.starmap(_ref_encode_worker, [(m, cache_path(m)) for m in todo])):
                 enc_s[m[0]] = round(dt, 1)
+    elif todo == []:
+        encoder = "cache/ (written by an earlier run; sha256-checked below)"
     ecs, hash_ok = {}, {}
     for m in wl["matrices"]:
         with open(cache_path(m), "rb") as fh:
             blob = fh.read()
         want = hashes.get(matrix_key(m), {}).get("sha256")
         hash_ok[m[0]] = (sha256(blob) == want) if want else None
+        if hash_ok[m[0]] is False:
+            raise SystemExit(f"{matrix_key(m)}: cached blob differs from the pinned reference encoding")
         ecs[m[0]] = storage.deserialize(blob)
     step_bytes = sum(model_bytes(ec) for ec in ecs.values())
     xs16 = launch_inputs(HEADLINE)
@@ -392,8 +409,7 @@ def run_reference(args):
                       "partial_y_summed": True, "rel_inf_vs_single_process": par_err,
                       "note": "secondary: each matrix's block sets split into groups, one process "
                               "each; step = slowest group + the partial-y sum"},
-        "inputs": {"encoder": "reference storage.convert_csr (baseline/_ref), cached in cache/",
-                   "encode_s": enc_s, "sha256_matches_pinned": hash_ok},
+        "inputs": {"encoder": encoder, "encode_s": enc_s, "sha256_matches_pinned": hash_ok},
         "native_so_loaded": libs,
     }
     print(json.dumps(line), flush=True)
@@ -1146,7 +1162,14 @@ def main():
     ap.add_argument("--shard", action="store_true", help="use the row-sharded path even at N=1")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="sharded y exchange: NVLink peer stores (one kernel) or NCCL all-gather")
+    ap.add_argument("--ref-inputs", default="native", choices=["reference", "native"],
+                    help="--impl reference: encode missing inputs with the reference pipeline or the "
+                         "native encoder in a separate process (both sha256-checked)")
+    ap.add_argument("--encode-cache", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.encode_cache:  # helper process of --ref-inputs native
+        load_workload(HEADLINE)
+        return
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
