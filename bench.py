@@ -706,7 +706,7 @@ def run_ours(args):
     spg = max(d for d in range(1, 9) if args.steps % d == 0)
     graph = wl.graph(stream, spg)  # one grouped launch per step
     with torch.cuda.stream(stream):
-        for _ in range(max(1, args.warmup // spg)):
+        for _ in range(max(3, -(-args.warmup // spg))):  # >= W warm-up steps (at least 15)
             graph.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

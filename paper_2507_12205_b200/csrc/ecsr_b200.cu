@@ -54,7 +54,7 @@ int tile_target() {
     const int v = env_int("ECSR_B200_TILE", 0);
     return t_tile_override ? t_tile_override : v ? std::max(1024, v) : g_tile_default;
 }
-int pre_tiles() { return std::max(1, env_int("ECSR_B200_PRE", 2)); }
+int pre_tiles() { return std::max(0, env_int("ECSR_B200_PRE", 2)); }
 bool trace_enabled() { return env_int("ECSR_B200_TRACE", 0) != 0; }
 bool trace_caller_resets() { return env_int("ECSR_B200_TRACE", 0) == 2; }
 bool coop_launch() { return env_int("ECSR_B200_COOP", 0) != 0; }

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 from paper_2507_12205_b200 import _lib  # noqa: E402
 
-_lib.LIB_PATH = os.path.join(ROOT, "build", "libtune.so")
+_lib.LIB_PATH = os.path.join(ROOT, "build", "libtune.so")  # ECSR_B200_PRE etc. apply
 import bench  # noqa: E402
 from paper_2507_12205_b200.device import spmv, to_device, vstack  # noqa: E402
 
