@@ -55,6 +55,11 @@ constexpr int kTickets = 3;     // tail-queue tickets a producer keeps in flight
 #define ECSR_CONSUMER_POLL_NS 64
 #endif
 constexpr unsigned kProducerPollNs = ECSR_PRODUCER_POLL_NS, kConsumerPollNs = ECSR_CONSUMER_POLL_NS;
+// Chunk-loop unroll of a group record (1: one chunk of every block per iteration).
+#ifndef ECSR_CHUNK_UNROLL
+#define ECSR_CHUNK_UNROLL 1
+#endif
+constexpr int kChunkUnroll = ECSR_CHUNK_UNROLL;
 constexpr int kMaxMembers = 8;  // matrices of one grouped launch
 
 // One matrix of a (grouped) launch: its packed arena and this launch's x and y.
@@ -468,7 +473,7 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
     float acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0f;
-#pragma unroll 1
+#pragma unroll kChunkUnroll
     for (uint32_t c = 0; c < nmin; ++c, ptr += P * (DCH + VCH)) {
         uint32_t d[P][(V + 3) / 4], w[P][NW];
 #ifdef ECSR_EXP_NOWEIGHTLDS
