@@ -60,6 +60,10 @@ constexpr unsigned kProducerPollNs = ECSR_PRODUCER_POLL_NS, kConsumerPollNs = EC
 #define ECSR_CHUNK_UNROLL 1
 #endif
 constexpr int kChunkUnroll = ECSR_CHUNK_UNROLL;
+#ifndef ECSR_GATE_LANE
+#define ECSR_GATE_LANE 0
+#endif
+constexpr int kGateLane = ECSR_GATE_LANE;  // producer lane that counts the CTA's zeroed slice
 constexpr int kMaxMembers = 8;  // matrices of one grouped launch
 
 // One matrix of a (grouped) launch: its packed arena and this launch's x and y.
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
             // only after the arrival, so launches on one workspace never mix generations.
             zero_slice(p, work, lane, 32);
             __syncwarp();
-            if (lane == 0) {
+            if (lane == kGateLane) {  // (ECSR_GATE_LANE: a lane that issued no bulk copies)
                 unsigned long long old;
                 asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.gate) : "memory");
                 atom_store_cta64(&gate_target, old - old % gridDim.x + gridDim.x + 1);
