@@ -59,9 +59,11 @@ bool trace_enabled() { return env_int("ECSR_B200_TRACE", 0) != 0; }
 bool trace_caller_resets() { return env_int("ECSR_B200_TRACE", 0) == 2; }
 bool coop_launch() { return env_int("ECSR_B200_COOP", 0) != 0; }
 bool group_force_cps1() { return env_int("ECSR_B200_GROUP_CPS1", 0) != 0; }
+bool pack_ffd() { return env_int("ECSR_B200_FFD", 1) != 0; }
 #else
 constexpr bool coop_launch() { return false; }
 constexpr bool group_force_cps1() { return false; }
+constexpr bool pack_ffd() { return true; }
 int tile_target() { return t_tile_override ? t_tile_override : g_tile_default; }
 int pre_tiles() { return 2; }  // tiles streamed before griddepcontrol.wait and the x copy
 constexpr bool trace_enabled() { return false; }
@@ -577,51 +579,81 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
             }
         si = se;
     }
-    // 2. pack records into tiles of <= tile_target() bytes
+    // 2. pack each run's records into tiles of <= tile_target() bytes, first-fit
+    //    decreasing: records keep whole-record granularity, so sequential packing leaves
+    //    a stage ~22 % empty on average (e.g. two 5.5 KB records in a 17 KB stage);
+    //    FFD fills ~89 % (a record's place is free: blocks are identified by slot).
     auto hdr_of = [](size_t n) { return round_up(8 + 2 * static_cast<int64_t>(n), 16); };
     for (const auto& run : runs) {
-        size_t i = 0;
-        while (i < run.size()) {
-            size_t n = 0;
-            int64_t bytes = 0;
-            while (i + n < run.size()) {
-                const int64_t rb = round_up(group_record_bytes(sets, run[i + n], wide), 16);
-                if (n > 0 && hdr_of(n + 1) + bytes + rb > tile_target()) break;
-                bytes += rb;
-                ++n;
+        std::vector<int64_t> rb(run.size());
+        for (size_t i = 0; i < run.size(); ++i) rb[i] = round_up(group_record_bytes(sets, run[i], wide), 16);
+        std::vector<std::vector<size_t>> bins;
+        std::vector<int64_t> bin_bytes;
+        if (pack_ffd()) {
+            std::vector<size_t> order(run.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+            std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return rb[x] > rb[y]; });
+            size_t first_open = 0;  // bins before it cannot take even the smallest record
+            const int64_t smallest = run.empty() ? 0 : *std::min_element(rb.begin(), rb.end());
+            for (size_t i : order) {
+                size_t bi = first_open;
+                for (; bi < bins.size(); ++bi)
+                    if (hdr_of(bins[bi].size() + 1) + bin_bytes[bi] + rb[i] <= tile_target()) break;
+                if (bi == bins.size()) {
+                    bins.emplace_back();
+                    bin_bytes.push_back(0);
+                }
+                bins[bi].push_back(i);
+                bin_bytes[bi] += rb[i];
+                while (first_open < bins.size() &&
+                       hdr_of(bins[first_open].size() + 1) + bin_bytes[first_open] + smallest > tile_target())
+                    ++first_open;
             }
+        } else {  // sequential (container order)
+            for (size_t i = 0; i < run.size(); ++i) {
+                if (bins.empty() || hdr_of(bins.back().size() + 1) + bin_bytes.back() + rb[i] > tile_target()) {
+                    bins.emplace_back();
+                    bin_bytes.push_back(0);
+                }
+                bins.back().push_back(i);
+                bin_bytes.back() += rb[i];
+            }
+        }
+        for (size_t bi = 0; bi < bins.size(); ++bi) {
+            const std::vector<size_t>& recs = bins[bi];
+            const size_t n = recs.size();
+            const int64_t bytes = bin_bytes[bi];
             const int64_t start = static_cast<int64_t>(arena->size());
             const int64_t hdr = hdr_of(n);
             arena->resize(start + hdr + bytes, 0);
             uint8_t* base = arena->data() + start;
             const uint32_t nrec = static_cast<uint32_t>(n);
             std::memcpy(base, &nrec, 4);
-            const ecsr_host_set& s0 = sets[run[i].blocks[0].first];
+            const ecsr_host_set& s0 = sets[run[recs[0]].blocks[0].first];
             const uint16_t gv = static_cast<uint16_t>((s0.granularity << 8) | s0.vector_size);
             std::memcpy(base + 4, &gv, 2);
-            const uint16_t p16 = static_cast<uint16_t>(run[i].P);
+            const uint16_t p16 = static_cast<uint16_t>(run[recs[0]].P);
             std::memcpy(base + 6, &p16, 2);
             int64_t off = hdr;
             double cost = 0;
             TileFeat tf;
             for (size_t k = 0; k < n; ++k) {
-                const GroupPlan& gp = run[i + k];
+                const GroupPlan& gp = run[recs[k]];
                 const int gc = gclass(sets[gp.blocks[0].first].granularity);
                 tf.rec[gc] += 1;
                 for (auto& sb : gp.blocks) tf.steps[gc] += static_cast<double>(block_chunks(sets[sb.first], sb.second));
                 tf.bytes += static_cast<double>(group_record_bytes(sets, gp, wide));
                 const uint16_t off16 = static_cast<uint16_t>(off / 16);
                 std::memcpy(base + 8 + 2 * k, &off16, 2);
-                write_group_record(sets, desc, run[i + k], host_dtype, wide, base + off);
-                off += round_up(group_record_bytes(sets, run[i + k], wide), 16);
-                cost += group_record_cost(sets, run[i + k], wide);
+                write_group_record(sets, desc, gp, host_dtype, wide, base + off);
+                off += rb[recs[k]];
+                cost += group_record_cost(sets, gp, wide);
             }
             tile_start16->push_back(static_cast<uint32_t>(start / 16));
             tile_rec_start->push_back(tile_rec_start->back() + static_cast<uint32_t>(n));
             tile_cost->push_back(cost);
             tile_feat->push_back(tf);
             *max_tile = std::max<int64_t>(*max_tile, hdr + bytes);
-            i += n;
         }
     }
     tile_start16->push_back(static_cast<uint32_t>(arena->size() / 16));

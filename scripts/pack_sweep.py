@@ -26,7 +26,7 @@ ys = [torch.empty(e.num_rows, device="cuda") for e in stacked]
 
 
 def run(env):
-    for k in ("ECSR_B200_TILE", "ECSR_B200_RECCAP"):
+    for k in ("ECSR_B200_TILE", "ECSR_B200_RECCAP", "ECSR_B200_RECMAX"):
         os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     Ws = [to_device(e) for e in stacked]
@@ -47,10 +47,10 @@ def run(env):
 
 
 run({})
-for env in [{"ECSR_B200_RECCAP": 6144}, {"ECSR_B200_RECCAP": 12288},
-            {"ECSR_B200_TILE": 15000}, {"ECSR_B200_TILE": 19000},
-            {"ECSR_B200_TILE": 6200, "ECSR_B200_RECCAP": 6200},
-            {"ECSR_B200_TILE": 8500, "ECSR_B200_RECCAP": 8500},
-            {"ECSR_B200_TILE": 11000, "ECSR_B200_RECCAP": 5500}]:
+for env in [{"ECSR_B200_TILE": 11000, "ECSR_B200_RECCAP": 8600, "ECSR_B200_RECMAX": 11000},
+            {"ECSR_B200_TILE": 13000, "ECSR_B200_RECCAP": 8600, "ECSR_B200_RECMAX": 13000},
+            {"ECSR_B200_TILE": 11000, "ECSR_B200_RECCAP": 11000, "ECSR_B200_RECMAX": 11000},
+            {"ECSR_B200_TILE": 13000, "ECSR_B200_RECCAP": 6500, "ECSR_B200_RECMAX": 13000},
+            {"ECSR_B200_RECMAX": 17000}]:
     run(env)
 run({})
