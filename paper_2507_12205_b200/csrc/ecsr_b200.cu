@@ -60,10 +60,12 @@ bool trace_caller_resets() { return env_int("ECSR_B200_TRACE", 0) == 2; }
 bool coop_launch() { return env_int("ECSR_B200_COOP", 0) != 0; }
 bool group_force_cps1() { return env_int("ECSR_B200_GROUP_CPS1", 0) != 0; }
 bool pack_ffd() { return env_int("ECSR_B200_FFD", 1) != 0; }
+bool pack_mixed() { return env_int("ECSR_B200_MIXED", 1) != 0; }
 #else
 constexpr bool coop_launch() { return false; }
 constexpr bool group_force_cps1() { return false; }
 constexpr bool pack_ffd() { return true; }
+constexpr bool pack_mixed() { return true; }
 int tile_target() { return t_tile_override ? t_tile_override : g_tile_default; }
 int pre_tiles() { return 2; }  // tiles streamed before griddepcontrol.wait and the x copy
 constexpr bool trace_enabled() { return false; }
@@ -579,11 +581,18 @@ void build_tiled_arena(const ecsr_host_set* sets, int nsets, const std::vector<S
             }
         si = se;
     }
-    // 2. pack each run's records into tiles of <= tile_target() bytes, first-fit
-    //    decreasing: records keep whole-record granularity, so sequential packing leaves
-    //    a stage ~22 % empty on average (e.g. two 5.5 KB records in a 17 KB stage);
-    //    FFD fills ~89 % (a record's place is free: blocks are identified by slot).
+    // 2. pack the records into tiles of <= tile_target() bytes, first-fit decreasing
+    //    over ALL runs (a tile may mix (g, v, P): the kernel dispatches on each record's
+    //    header): records keep whole-record granularity, so sequential per-run packing
+    //    left a stage ~22 % empty on average (two 5.5 KB records in a 17 KB stage); FFD
+    //    over mixed runs fills ~95 % (a record's place is free: blocks are identified by
+    //    their slot).
     auto hdr_of = [](size_t n) { return round_up(8 + 2 * static_cast<int64_t>(n), 16); };
+    if (pack_mixed()) {  // one pool of every run's records: tiles may mix (g, v, P)
+        std::vector<GroupPlan> all;
+        for (const auto& run : runs) all.insert(all.end(), run.begin(), run.end());
+        runs.assign(1, all);
+    }
     for (const auto& run : runs) {
         std::vector<int64_t> rb(run.size());
         for (size_t i = 0; i < run.size(); ++i) rb[i] = round_up(group_record_bytes(sets, run[i], wide), 16);
@@ -1072,17 +1081,22 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                           &d->tile_feat, &max_tile);
         // the lean kernel covers v = 4 runs with the default blocks-per-record (or half
         // of it for g = 2, down to a quarter for g = 1) and g <= 8, and v = 1 runs of g = 1 (the reference's short set)
-        d->lean = true;
-        for (int64_t t = 0; t + 1 < static_cast<int64_t>(tstart.size()); ++t) {
+        d->lean = true;  // every record's (g, v, P) has a lean-kernel variant
+        for (int64_t t = 0; t + 1 < static_cast<int64_t>(tstart.size()) && d->lean; ++t) {
             const uint8_t* th = arena.data() + 16ull * tstart[t];
-            uint16_t gv, pp;
-            std::memcpy(&gv, th + 4, 2);
-            std::memcpy(&pp, th + 6, 2);
-            const int g = gv >> 8, v = gv & 0xff;
-            const bool ok = (v == 4 && g <= 8 &&
-                             (pp == group_p(g) || (g <= 2 && 2 * pp == group_p(g)) || (g == 1 && 4 * pp == group_p(g)))) ||
-                            (v == 1 && g == 1);
-            if (!ok) d->lean = false;
+            uint32_t nrec;
+            std::memcpy(&nrec, th, 4);
+            for (uint32_t jr = 0; jr < nrec; ++jr) {
+                uint16_t off16;
+                std::memcpy(&off16, th + 8 + 2 * jr, 2);
+                const uint8_t* rh = th + 16 * off16;
+                const int g = rh[50], v = rh[51], pp = rh[54];
+                const bool ok = (v == 4 && g <= 8 &&
+                                 (pp == group_p(g) || (g <= 2 && 2 * pp == group_p(g)) ||
+                                  (g == 1 && 4 * pp == group_p(g)))) ||
+                                (v == 1 && g == 1);
+                if (!ok) d->lean = false;
+            }
         }
         const int64_t stage = round_up(std::max<int64_t>(max_tile, tile_target()), 128);
         d->ctas_per_sm = ctas_per_sm;  // CTAs share the SM's 228 KB (1 KB reserved each)

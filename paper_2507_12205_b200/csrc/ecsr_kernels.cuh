@@ -440,8 +440,8 @@ __device__ __forceinline__ void emit_row(uint32_t r, int g, int P, int blk, int 
 // `next` runs once per record, right before the lane reduction: the consumer loop claims
 // its next record there, so the claim's round trip overlaps the shuffles.
 template <int G, int V, int P, class Next>
-__device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int lane, const RecCtx& p,
-                                                   YGate& gate, Next&& next) {
+__device__ __forceinline__ void tiled_group_record(uint32_t r, const uint32_t (&m)[2], uint32_t xs, int lane,
+                                                   const RecCtx& p, YGate& gate, Next&& next) {
     constexpr int NACC = P * G;
     constexpr int kStride = 32 / NACC;
     const int a = lane / kStride;  // accumulator a after the reduce-scatter: block a / G, row a % G
@@ -449,8 +449,6 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
     // header, lane bases and the lane's output row (or partial slot) are independent
     // shared loads: issue them together so their latencies overlap
     const uint32_t q = r + group_header_bytes(G, P);
-    uint32_t m[2];
-    lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present
     uint32_t out_idx;
     lds_bytes<4>(p.tp->ordered ? r + 4 * blk : r + 64 + 4 * (blk * G + k), &out_idx);
     uint32_t xa[P];
@@ -524,11 +522,9 @@ __device__ __forceinline__ void tiled_group_record(uint32_t r, uint32_t xs, int 
 // A single-block record of g = 8 * passes rows (g in {16, 32}): one walk per pass of
 // 8 rows; a column's g values are contiguous, so a pass reads one 16-byte slice.
 template <int V, class Next>
-__device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs, int lane,
+__device__ __forceinline__ void tiled_wide_record(uint32_t r, const uint32_t (&m)[2], int g, uint32_t xs, int lane,
                                                   const RecCtx& p, YGate& gate, Next&& next) {
     constexpr int G = 8;
-    uint32_t m[2];
-    lds_bytes<8>(r + 48, m);
     next();
     const uint32_t nch = m[0] & 0xffffu, present = (m[1] >> 8) & 0xffu;
     if (!present) return;
@@ -571,51 +567,54 @@ __device__ __forceinline__ void tiled_wide_record(uint32_t r, int g, uint32_t xs
 // kFull: every (g, v, P) record variant; otherwise only the common ones (v = 4 with
 // the default P, or half of it for g = 2, or down to a quarter for g = 1; v = 1 with g = 1) -- a smaller kernel body keeps the instruction
 // cache warm; the packer picks the lean kernel when the container needs nothing else.
+// Dispatch on the record's own (g, v, P) (header bytes 50, 51, 54): a tile may mix runs.
 template <bool kFull, class Next>
-__device__ __forceinline__ void tiled_record(uint32_t r, uint32_t gv, uint32_t P, uint32_t xs, int lane,
+__device__ __forceinline__ void tiled_record(uint32_t r, const uint32_t (&m)[2], uint32_t xs, int lane,
                                              const RecCtx& p, YGate& gate, Next&& next) {
+    const uint32_t gv = ((m[0] >> 8) & 0xff00u) | (m[0] >> 24);  // g << 8 | v
+    const uint32_t P = (m[1] >> 16) & 0xffu;
     const int g = static_cast<int>(gv >> 8);
     const bool v4 = (gv & 0xffu) == 4;
     if constexpr (!kFull) {
         if (!v4) {
-            tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate, next);
+            tiled_group_record<1, 1, group_blocks(1)>(r, m, xs, lane, p, gate, next);
             return;
         }
         switch (g) {
             case 1:
-                if (P == group_blocks(1)) tiled_group_record<1, 4, group_blocks(1)>(r, xs, lane, p, gate, next);
-                else if (P == group_blocks(1) / 2) tiled_group_record<1, 4, group_blocks(1) / 2>(r, xs, lane, p, gate, next);
-                else tiled_group_record<1, 4, group_blocks(1) / 4>(r, xs, lane, p, gate, next);
+                if (P == group_blocks(1)) tiled_group_record<1, 4, group_blocks(1)>(r, m, xs, lane, p, gate, next);
+                else if (P == group_blocks(1) / 2) tiled_group_record<1, 4, group_blocks(1) / 2>(r, m, xs, lane, p, gate, next);
+                else tiled_group_record<1, 4, group_blocks(1) / 4>(r, m, xs, lane, p, gate, next);
                 break;
             case 2:
-                if (P == group_blocks(2)) tiled_group_record<2, 4, group_blocks(2)>(r, xs, lane, p, gate, next);
-                else tiled_group_record<2, 4, group_blocks(2) / 2>(r, xs, lane, p, gate, next);
+                if (P == group_blocks(2)) tiled_group_record<2, 4, group_blocks(2)>(r, m, xs, lane, p, gate, next);
+                else tiled_group_record<2, 4, group_blocks(2) / 2>(r, m, xs, lane, p, gate, next);
                 break;
-            case 4: tiled_group_record<4, 4, group_blocks(4)>(r, xs, lane, p, gate, next); break;
-            default: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate, next); break;
+            case 4: tiled_group_record<4, 4, group_blocks(4)>(r, m, xs, lane, p, gate, next); break;
+            default: tiled_group_record<8, 4, 1>(r, m, xs, lane, p, gate, next); break;
         }
         return;
     }
     if (!v4) {  // short 1-grained sets (v = 1, storage.py:99-122) and other narrow blocks
-        if (g == 1) tiled_group_record<1, 1, group_blocks(1)>(r, xs, lane, p, gate, next);
-        else if (g == 2) tiled_group_record<2, 1, group_blocks(2)>(r, xs, lane, p, gate, next);
-        else if (g == 4) tiled_group_record<4, 1, group_blocks(4)>(r, xs, lane, p, gate, next);
-        else if (g == 8) tiled_group_record<8, 1, 1>(r, xs, lane, p, gate, next);
-        else tiled_wide_record<1>(r, g, xs, lane, p, gate, next);
+        if (g == 1) tiled_group_record<1, 1, group_blocks(1)>(r, m, xs, lane, p, gate, next);
+        else if (g == 2) tiled_group_record<2, 1, group_blocks(2)>(r, m, xs, lane, p, gate, next);
+        else if (g == 4) tiled_group_record<4, 1, group_blocks(4)>(r, m, xs, lane, p, gate, next);
+        else if (g == 8) tiled_group_record<8, 1, 1>(r, m, xs, lane, p, gate, next);
+        else tiled_wide_record<1>(r, m, g, xs, lane, p, gate, next);
         return;
     }
     switch ((g << 4) | P) {  // (g, blocks per record) of this run (packer: kRecordCap)
-        case (1 << 4) | 8: tiled_group_record<1, 4, 8>(r, xs, lane, p, gate, next); break;
-        case (1 << 4) | 4: tiled_group_record<1, 4, 4>(r, xs, lane, p, gate, next); break;
-        case (1 << 4) | 2: tiled_group_record<1, 4, 2>(r, xs, lane, p, gate, next); break;
-        case (1 << 4) | 1: tiled_group_record<1, 4, 1>(r, xs, lane, p, gate, next); break;
-        case (2 << 4) | 4: tiled_group_record<2, 4, 4>(r, xs, lane, p, gate, next); break;
-        case (2 << 4) | 2: tiled_group_record<2, 4, 2>(r, xs, lane, p, gate, next); break;
-        case (2 << 4) | 1: tiled_group_record<2, 4, 1>(r, xs, lane, p, gate, next); break;
-        case (4 << 4) | 2: tiled_group_record<4, 4, 2>(r, xs, lane, p, gate, next); break;
-        case (4 << 4) | 1: tiled_group_record<4, 4, 1>(r, xs, lane, p, gate, next); break;
-        case (8 << 4) | 1: tiled_group_record<8, 4, 1>(r, xs, lane, p, gate, next); break;
-        default: tiled_wide_record<4>(r, g, xs, lane, p, gate, next); break;  // g = 16, 32
+        case (1 << 4) | 8: tiled_group_record<1, 4, 8>(r, m, xs, lane, p, gate, next); break;
+        case (1 << 4) | 4: tiled_group_record<1, 4, 4>(r, m, xs, lane, p, gate, next); break;
+        case (1 << 4) | 2: tiled_group_record<1, 4, 2>(r, m, xs, lane, p, gate, next); break;
+        case (1 << 4) | 1: tiled_group_record<1, 4, 1>(r, m, xs, lane, p, gate, next); break;
+        case (2 << 4) | 4: tiled_group_record<2, 4, 4>(r, m, xs, lane, p, gate, next); break;
+        case (2 << 4) | 2: tiled_group_record<2, 4, 2>(r, m, xs, lane, p, gate, next); break;
+        case (2 << 4) | 1: tiled_group_record<2, 4, 1>(r, m, xs, lane, p, gate, next); break;
+        case (4 << 4) | 2: tiled_group_record<4, 4, 2>(r, m, xs, lane, p, gate, next); break;
+        case (4 << 4) | 1: tiled_group_record<4, 4, 1>(r, m, xs, lane, p, gate, next); break;
+        case (8 << 4) | 1: tiled_group_record<8, 4, 1>(r, m, xs, lane, p, gate, next); break;
+        default: tiled_wide_record<4>(r, m, g, xs, lane, p, gate, next); break;  // g = 16, 32
     }
 }
 
@@ -893,12 +892,12 @@ __global__ void __launch_bounds__(tiled_threads(NC), kConsumerWarpsPerSm / NC)
 #endif
         ECSR_TRACE(3, threadIdx.x == 0 && ti == 0);
         const uint32_t tile = stages_addr + stage * stage_bytes + tok;  // reads after the fill
-        uint32_t th[2];
-        lds_bytes<8>(tile, th);
-        const uint32_t gv = th[1] & 0xffffu;
         uint32_t off16;
         lds_bytes<2>(tile + 8 + 2 * (k - tile_begin), &off16);
-        tiled_record<kFull>(tile + 16u * (off16 & 0xffffu), gv, th[1] >> 16, xs_addr, lane, rc, gate, claim_next);
+        const uint32_t r = tile + 16u * (off16 & 0xffffu);
+        uint32_t m[2];
+        lds_bytes<8>(r + 48, m);  // nmin | g | v ; nblk | present | P | has_tail
+        tiled_record<kFull>(r, m, xs_addr, lane, rc, gate, claim_next);
 #ifdef ECSR_TRACE_CYCLES
         cyc_work += clock64() - c1;
         ++nwork;
