@@ -76,10 +76,10 @@ constexpr int kMaxStages = 16;
 constexpr int kPackInternal = 1 << 30;  // spmv_set: unbounded u32 deltas (validated by range)
 constexpr double kQueueShare = 0.05;       // cost share of each CTA's range drawn from the tail
                                            // queue: a single matrix's launch
-constexpr double kGroupQueueShare = 0.30;  // the same for a grouped launch (one tail per step,
-                                           // members' CTAs sharing SMs: measured best 0.30)
+constexpr double kGroupQueueShare = 0.40;  // the same for a grouped launch (one tail per step,
+                                           // members' CTAs sharing SMs: measured best 0.35-0.45)
 #ifdef ECSR_B200_TUNING
-double group_queue_share() { return env_int("ECSR_B200_GROUP_QPCT", 30) / 100.0; }
+double group_queue_share() { return env_int("ECSR_B200_GROUP_QPCT", 40) / 100.0; }
 #else
 double group_queue_share() { return kGroupQueueShare; }
 #endif
