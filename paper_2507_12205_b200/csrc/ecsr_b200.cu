@@ -72,6 +72,10 @@ constexpr bool trace_enabled() { return false; }
 constexpr bool trace_caller_resets() { return false; }
 #endif
 constexpr int kMaxStageBytes = 65536;   // largest tile a ring slot may hold
+#ifndef ECSR_SMEM_RESERVE
+#define ECSR_SMEM_RESERVE 4096
+#endif
+constexpr int64_t kSmemReserve = ECSR_SMEM_RESERVE;  // static shared memory (~1 KB) + margin
 constexpr int kMaxStages = 16;
 constexpr int kPackInternal = 1 << 30;  // spmv_set: unbounded u32 deltas (validated by range)
 constexpr double kQueueShare = 0.05;       // cost share of each CTA's range drawn from the tail
@@ -1067,7 +1071,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
         // ~32 KB (1 CTA), stretched so that a whole number of them uses all of it
         // (more bytes in flight per SM; e.g. 5 x 18.3 KB instead of 5 x 16 KB at K = 8192).
         const int64_t cta_smem = ctas_per_sm == 1 ? lim.smem_optin : (lim.smem_per_sm / ctas_per_sm) - 1024;
-        const int64_t avail = cta_smem - 4096 - 16 * kMaxStages - xbytes;  // static smem + barriers
+        const int64_t avail = cta_smem - kSmemReserve - 16 * kMaxStages - xbytes;  // static smem + barriers
         {
             const int64_t base = ctas_per_sm == 2 ? 16384 : 32768;
             const int64_t n0 = std::min<int64_t>(kMaxStages, std::max<int64_t>(2, avail / base));
@@ -1352,7 +1356,7 @@ int plan_part(const std::vector<const ecsr_dev*>& mats, const DeviceLimits& lim,
         int nst = d->nstages, smem = d->smem_bytes;
         if (d->ctas_per_sm != pt->cps) {  // a two-CTA member in a one-CTA launch: deepen its pool
             const int64_t xbytes = round_up(2 * std::max<int64_t>(d->K, 1), 16);
-            const int64_t avail = lim.smem_optin - 4096 - 16 * kMaxStages - xbytes;
+            const int64_t avail = lim.smem_optin - kSmemReserve - 16 * kMaxStages - xbytes;
             nst = static_cast<int>(std::min<int64_t>(kMaxStages, avail / std::max(d->stage_bytes, 1)));
             smem = static_cast<int>(round_up(8 * nst + 8, 128) + int64_t{nst} * d->stage_bytes + xbytes);
         }
