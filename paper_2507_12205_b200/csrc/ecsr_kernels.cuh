@@ -45,7 +45,10 @@ namespace ecsr {
 constexpr int kConsumerWarpsPerSm = ECSR_CONSUMER_WARPS_PER_SM;
 __host__ __device__ constexpr int tiled_threads(int nc) { return 32 * (nc + 1); }
 constexpr int kMaxRingStages = 16;
-constexpr int kTickets = 3;     // tail-queue tickets a producer keeps in flight
+#ifndef ECSR_TICKETS
+#define ECSR_TICKETS 3
+#endif
+constexpr int kTickets = ECSR_TICKETS;  // tail-queue tickets a producer keeps in flight
 // Back-off of the producer's stage-pool poll and of a consumer waiting for its record's
 // tile to be issued (tuning builds may override them).
 #ifndef ECSR_PRODUCER_POLL_NS
