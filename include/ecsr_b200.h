@@ -197,6 +197,20 @@ int ecsr_b200_parse(const uint8_t* blob, int64_t len, ecsr_blob_info* info);
 int ecsr_b200_load(const uint8_t* blob, int64_t len, int32_t device_dtype, int32_t flags,
                    ecsr_dev** out);
 
+/* Host-side (de)serialization of the wire format, the reference's storage.serialize /
+ * deserialize (storage.py:389-483): ecsr_b200_blob_open parses and shape-checks like
+ * ecsr_b200_parse and keeps the sets on the host; _set_info sizes the caller's arrays and
+ * _copy_set fills them (values in the blob's f32/f64). ecsr_b200_serialize writes a
+ * container byte-identical to storage.serialize (call with out = NULL to size it). */
+typedef struct ecsr_blob ecsr_blob;
+int ecsr_b200_blob_open(const uint8_t* blob, int64_t len, ecsr_blob** out);
+int ecsr_b200_blob_header(const ecsr_blob* blob, ecsr_blob_info* info);
+int ecsr_b200_blob_set_info(const ecsr_blob* blob, int32_t set, ecsr_set_info* info);
+int ecsr_b200_blob_copy_set(const ecsr_blob* blob, int32_t set, ecsr_out_set* out);
+void ecsr_b200_blob_free(ecsr_blob* blob);
+int ecsr_b200_serialize(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, int64_t num_cols,
+                        int32_t warp_size, int32_t delta_bits, int32_t value_bits, int32_t value_dtype,
+                        uint8_t* out, int64_t cap, int64_t* len);
 int ecsr_b200_info(const ecsr_dev* dev, int64_t* num_rows, int64_t* num_cols, int32_t* nsets,
                    int32_t* warp_size, int32_t* delta_bits, int32_t* value_bits,
                    int32_t* device_dtype);

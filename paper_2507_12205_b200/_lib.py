@@ -80,6 +80,13 @@ SIGNATURES = {
     "ecsr_b200_unpack": (c_i32, [c_vp, ctypes.POINTER(OutSet), c_i32, c_i32]),
     "ecsr_b200_bytes": (c_i32, [c_vp, ctypes.POINTER(Bytes)]),
     "ecsr_b200_free": (None, [c_vp]),
+    "ecsr_b200_blob_open": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "ecsr_b200_blob_header": (c_i32, [c_vp, ctypes.POINTER(BlobInfo)]),
+    "ecsr_b200_blob_set_info": (c_i32, [c_vp, c_i32, ctypes.POINTER(SetInfo)]),
+    "ecsr_b200_blob_copy_set": (c_i32, [c_vp, c_i32, ctypes.POINTER(OutSet)]),
+    "ecsr_b200_blob_free": (None, [c_vp]),
+    "ecsr_b200_serialize": (c_i32, [ctypes.POINTER(HostSet), c_i32, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32,
+                                    c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "ecsr_b200_group_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, ctypes.POINTER(c_vp)]),
     "ecsr_b200_group_spmv": (c_i32, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i32, c_vp]),
     "ecsr_b200_group_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),

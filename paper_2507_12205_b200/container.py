@@ -6,7 +6,8 @@ GPU box needs no reference install:
 * `EcCsrSet` / `EcCsrMatrix` -- same fields, dtypes and meaning as
   `storage.py:50-96` (duck-type compatible: the packer accepts either class).
 * `serialize` / `deserialize` -- the `.ecsr` format of `storage.py:16-31`,
-  `389-483`, byte-identical (tests check `serialize` equality both ways).
+  `389-483`, byte-identical (tests check `serialize` equality both ways); the bytes are
+  written and parsed by the native library (`ecsr_b200_serialize`, `ecsr_b200_blob_*`).
 * `storage_report` components and `kernel_model_bytes` -- the byte model of
   `storage.py:579-649`; the roofline numerator of SURVEY.md §8(d) is
   `kernel_model_bytes` (components minus pad_mask and desc, plus x and y).
@@ -82,127 +83,98 @@ class EcCsrMatrix:
                            self.delta_bits, self.warp_size, sets)
 
 
-# --- wire format (storage.py:335-483) ---------------------------------------
+# --- wire format (storage.py:389-483): native, libecsr_b200.so -----------------------
 
 
 def _delta_bytes(count: int, bits: int) -> int:
-    if bits == 4:
-        return (count + 1) // 2
-    return count * (bits // 8)
+    """Packed size of `count` deltas of `bits` bits (4-bit deltas share bytes)."""
+    return (count * bits + 7) // 8
 
 
-def _pack_deltas(deltas: np.ndarray, bits: int) -> bytes:
-    if deltas.size and int(deltas.max()) >= (1 << bits):
-        raise ContainerError(f"delta exceeds {bits}-bit range")
-    if bits == 4:
-        d = deltas.astype(np.uint8)
-        if d.size % 2:
-            d = np.concatenate((d, np.zeros(1, dtype=np.uint8)))
-        return (d[0::2] | (d[1::2] << 4)).tobytes()
-    if bits == 8:
-        return deltas.astype(np.uint8).tobytes()
-    return deltas.astype("<u2").tobytes()
+def host_sets(ec, check_shapes: bool = True):
+    """Coerce a container's sets to the C-ABI dtypes (copies only on mismatch, like
+    np.ascontiguousarray in `_speedups.pyx:62-77`). Returns (HostSet array, keepalive,
+    value dtype). Array lengths are checked against the declared sizes first
+    (`storage.py:312-329`): the native side trusts num_blocks / stored_cols."""
+    from . import _lib
 
-
-def _unpack_deltas(buf: bytes, count: int, bits: int) -> np.ndarray:
-    raw = np.frombuffer(buf, dtype=np.uint8)
-    if bits == 4:
-        out = np.empty(raw.size * 2, dtype=np.uint32)
-        out[0::2] = raw & 0x0F
-        out[1::2] = raw >> 4
-        return out[:count].copy()
-    if bits == 8:
-        return raw.astype(np.uint32)
-    return np.frombuffer(buf, dtype="<u2").astype(np.uint32)
+    dtype = np.dtype(ec.dtype)
+    if dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
+        raise ValueError("container values must be float32 or float64")
+    keep = []
+    arr = (_lib.HostSet * max(len(ec.sets), 1))()
+    for s in ec.sets if check_shapes else ():
+        check_set_shapes(s, int(ec.warp_size))
+    for i, s in enumerate(ec.sets):
+        rows = np.ascontiguousarray(s.row_indices, dtype=np.uint32)
+        indptr = np.ascontiguousarray(s.block_indptr, dtype=np.int64)
+        bases = np.ascontiguousarray(s.base_indices, dtype=np.uint32)
+        deltas = np.ascontiguousarray(s.delta_indices, dtype=np.uint32)
+        mask = np.ascontiguousarray(s.pad_mask, dtype=np.bool_).view(np.uint8)
+        vals = np.ascontiguousarray(s.block_values, dtype=dtype)
+        keep += [rows, indptr, bases, deltas, mask, vals]
+        arr[i] = _lib.HostSet(int(s.granularity), int(s.vector_size), int(s.num_blocks),
+                              int(s.stored_cols), int(s.real_nnz), _lib.ptr(rows),
+                              _lib.ptr(indptr), _lib.ptr(bases), _lib.ptr(deltas),
+                              _lib.ptr(mask), _lib.ptr(vals))
+    return arr, keep, dtype
 
 
 def serialize(ec) -> bytes:
-    """Byte-identical to `ecsr.storage.serialize` (`storage.py:389-428`)."""
-    dtype = np.dtype(ec.dtype)
-    parts = [MAGIC, struct.pack(_HEADER_FMT, VERSION, dtype.itemsize, ec.value_bits,
-                                ec.delta_bits, ec.warp_size, ec.num_rows, ec.num_cols,
-                                len(ec.sets))]
-    for s in ec.sets:
-        parts.append(struct.pack(_DESC_FMT, s.granularity, s.vector_size, s.num_blocks,
-                                 s.stored_cols, s.real_nnz))
-        for arr, dt in ((s.row_indices, "<u4"), (s.block_indptr, "<u8"),
-                        (s.base_indices, "<u4")):
-            a = np.ascontiguousarray(arr).astype(dt)
-            parts.append(struct.pack("<Q", a.size))
-            parts.append(a.tobytes())
-        parts.append(struct.pack("<Q", s.delta_indices.size))
-        parts.append(_pack_deltas(np.asarray(s.delta_indices), ec.delta_bits))
-        parts.append(struct.pack("<Q", s.pad_mask.size))
-        parts.append(np.packbits(np.asarray(s.pad_mask).astype(np.uint8),
-                                 bitorder="little").tobytes())
-        vals = np.ascontiguousarray(s.block_values, dtype=dtype.newbyteorder("<"))
-        parts.append(struct.pack("<Q", vals.size))
-        parts.append(vals.tobytes())
-    return b"".join(parts)
+    """Byte-identical to `ecsr.storage.serialize` (`storage.py:389-428`), written by
+    `ecsr_b200_serialize`."""
+    import ctypes
 
+    from . import _lib
 
-class _Reader:
-    def __init__(self, data: bytes):
-        self.data = memoryview(data)
-        self.pos = 0
-
-    def take(self, n: int, what: str) -> bytes:
-        if self.pos + n > len(self.data):
-            raise ContainerError(
-                f"truncated container: needed {n} bytes for {what} at offset {self.pos}")
-        out = self.data[self.pos:self.pos + n]
-        self.pos += n
-        return out
-
-    def unpack(self, fmt: str, what: str):
-        return struct.unpack(fmt, self.take(struct.calcsize(fmt), what))
-
-    def array(self, dtype, what: str) -> np.ndarray:
-        (count,) = self.unpack("<Q", what + " length")
-        dt = np.dtype(dtype)
-        return np.frombuffer(self.take(count * dt.itemsize, what), dtype=dt).copy()
+    arr, keep, dtype = host_sets(ec)
+    args = (arr, len(ec.sets), int(ec.num_rows), int(ec.num_cols), int(ec.warp_size), int(ec.delta_bits),
+            int(ec.value_bits), _lib.dtype_code(dtype))
+    n = ctypes.c_int64(0)
+    _lib.check(_lib.lib().ecsr_b200_serialize(*args, None, 0, ctypes.byref(n)), "ecsr_b200_serialize")
+    buf = ctypes.create_string_buffer(max(n.value, 1))
+    _lib.check(_lib.lib().ecsr_b200_serialize(*args, buf, n.value, ctypes.byref(n)), "ecsr_b200_serialize")
+    del keep
+    return buf.raw[:n.value]
 
 
 def deserialize(data: bytes) -> EcCsrMatrix:
-    """Parse and reject corruption exactly as `storage.py:431-483` does."""
-    rd = _Reader(data)
-    if bytes(rd.take(4, "magic")) != MAGIC:
-        raise ContainerError("bad magic: not an ECSR container")
-    version, vsize, vbits, dbits, warp, rows, cols, nsets = rd.unpack(_HEADER_FMT, "header")
-    if version != VERSION:
-        raise ContainerError(f"unsupported container version {version}")
-    if vsize not in (4, 8):
-        raise ContainerError(f"unsupported value width {vsize}")
-    if vbits not in (16, 32, 64):
-        raise ContainerError(f"unsupported value precision tag {vbits}")
-    if dbits not in (4, 8, 16):
-        raise ContainerError(f"unsupported delta precision {dbits}")
-    if warp < 1:
-        raise ContainerError("warp size must be positive")
-    dtype = np.dtype(np.float32 if vsize == 4 else np.float64)
-    sets = []
-    for _ in range(nsets):
-        g, v, num_blocks, stored, real = rd.unpack(_DESC_FMT, "set descriptor")
-        if g < 1 or v < 1:
-            raise ContainerError("set granularity and vector size must be positive")
-        row_indices = rd.array("<u4", "row_indices")
-        block_indptr = rd.array("<u8", "block_indptr").astype(np.int64)
-        base_indices = rd.array("<u4", "base_indices")
-        (dcount,) = rd.unpack("<Q", "delta_indices length")
-        deltas = _unpack_deltas(rd.take(_delta_bytes(dcount, dbits), "delta_indices"),
-                                dcount, dbits)
-        (mcount,) = rd.unpack("<Q", "pad_mask length")
-        mask_bytes = rd.take((mcount + 7) // 8, "pad_mask")
-        mask = np.unpackbits(np.frombuffer(mask_bytes, dtype=np.uint8), count=mcount,
-                             bitorder="little").astype(bool)
-        values = rd.array(dtype.newbyteorder("<"), "block_values").astype(dtype)
-        s = EcCsrSet(int(g), int(v), int(num_blocks), int(stored), int(real), row_indices,
-                     block_indptr, base_indices, deltas, mask, values)
-        check_set_shapes(s, warp)
-        sets.append(s)
-    if rd.pos != len(data):
-        raise ContainerError(f"{len(data) - rd.pos} trailing bytes after container")
-    return EcCsrMatrix(int(rows), int(cols), vbits, dbits, warp, sets)
+    """Parse and reject corruption exactly as `storage.py:431-483` does (the native
+    parser `ecsr_b200_blob_open`: same checks, same ContainerError messages)."""
+    import ctypes
+
+    from . import _lib
+
+    lib = _lib.lib()
+    data = bytes(data)
+    buf = ctypes.create_string_buffer(data, len(data))
+    h = ctypes.c_void_p()
+    rc = lib.ecsr_b200_blob_open(buf, len(data), ctypes.byref(h))
+    if rc == _lib.ERR_CONTAINER:  # the reference's message, unprefixed (storage.py:431-483)
+        raise ContainerError(_lib.last_error())
+    _lib.check(rc, "deserialize")
+    try:
+        info = _lib.BlobInfo()
+        _lib.check(lib.ecsr_b200_blob_header(h, ctypes.byref(info)), "deserialize")
+        dtype = np.dtype(np.float32 if info.value_bytes == 4 else np.float64)
+        warp = int(info.warp_size)
+        sets = []
+        for i in range(info.nsets):
+            si = _lib.SetInfo()
+            _lib.check(lib.ecsr_b200_blob_set_info(h, i, ctypes.byref(si)), "deserialize")
+            g, nb, st = int(si.granularity), int(si.num_blocks), int(si.stored_cols)
+            arrs = [np.empty(nb * g, np.uint32), np.empty(max(nb + 1, 1), np.int64),
+                    np.empty(nb * warp, np.uint32), np.empty(st, np.uint32), np.empty(st, np.uint8),
+                    np.empty(st * g, dtype)]
+            out = _lib.OutSet(*[a.ctypes.data for a in arrs])
+            _lib.check(lib.ecsr_b200_blob_copy_set(h, i, ctypes.byref(out)), "deserialize")
+            rows, indptr, bases, deltas, mask, vals = arrs
+            sets.append(EcCsrSet(g, int(si.vector_size), nb, st, int(si.real_nnz), rows, indptr, bases,
+                                 deltas, mask.astype(bool), vals))
+    finally:
+        lib.ecsr_b200_blob_free(h)
+    return EcCsrMatrix(int(info.num_rows), int(info.num_cols), int(info.value_bits), int(info.delta_bits),
+                       warp, sets)
 
 
 def save_container(ec, path) -> None:

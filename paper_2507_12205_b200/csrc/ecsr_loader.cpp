@@ -238,4 +238,147 @@ int ecsr_b200_load(const uint8_t* blob, int64_t len, int32_t device_dtype, int32
                           device_dtype, flags, out);
 }
 
+// A parsed blob held on the host: the sets as the reference arrays (deserialize).
+struct ecsr_blob {
+    Parsed P;
+};
+
+int ecsr_b200_blob_open(const uint8_t* blob, int64_t len, ecsr_blob** out) {
+    if (!out) return set_error(ECSR_ERR_VALUE, "null output handle");
+    *out = nullptr;
+    auto* b = new ecsr_blob();
+    if (int rc = parse(blob, len, &b->P)) {
+        delete b;
+        return rc;
+    }
+    *out = b;
+    return ECSR_OK;
+}
+
+int ecsr_b200_blob_header(const ecsr_blob* b, ecsr_blob_info* info) {
+    if (!b || !info) return set_error(ECSR_ERR_VALUE, "null argument");
+    const Parsed& P = b->P;
+    *info = ecsr_blob_info{};
+    info->num_rows = static_cast<int64_t>(P.rows);
+    info->num_cols = static_cast<int64_t>(P.cols);
+    info->nsets = static_cast<int32_t>(P.nsets);
+    info->warp_size = P.warp;
+    info->delta_bits = P.dbits;
+    info->value_bits = P.vbits;
+    info->value_bytes = P.vsize;
+    for (const auto& s : P.sets) {
+        info->stored_cols += static_cast<int64_t>(s.stored);
+        info->num_blocks += static_cast<int64_t>(s.nb);
+        info->real_nnz += static_cast<int64_t>(s.real);
+    }
+    return ECSR_OK;
+}
+
+int ecsr_b200_blob_set_info(const ecsr_blob* b, int32_t set, ecsr_set_info* info) {
+    if (!b || !info) return set_error(ECSR_ERR_VALUE, "null argument");
+    if (set < 0 || set >= static_cast<int32_t>(b->P.sets.size())) return set_error(ECSR_ERR_VALUE, "set index");
+    const ParsedSet& s = b->P.sets[set];
+    info->granularity = static_cast<int32_t>(s.g);
+    info->vector_size = static_cast<int32_t>(s.v);
+    info->num_blocks = static_cast<int64_t>(s.nb);
+    info->stored_cols = static_cast<int64_t>(s.stored);
+    info->real_nnz = static_cast<int64_t>(s.real);
+    return ECSR_OK;
+}
+
+int ecsr_b200_blob_copy_set(const ecsr_blob* b, int32_t set, ecsr_out_set* out) {
+    if (!b || !out) return set_error(ECSR_ERR_VALUE, "null argument");
+    if (set < 0 || set >= static_cast<int32_t>(b->P.sets.size())) return set_error(ECSR_ERR_VALUE, "set index");
+    const ParsedSet& s = b->P.sets[set];
+    auto put = [](void* dst, const void* src, size_t bytes) {
+        if (bytes) std::memcpy(dst, src, bytes);
+    };
+    put(out->row_indices, s.rows.data(), 4 * s.rows.size());
+    put(out->block_indptr, s.indptr.data(), 8 * s.indptr.size());
+    put(out->base_indices, s.bases.data(), 4 * s.bases.size());
+    put(out->delta_indices, s.deltas.data(), 4 * s.deltas.size());
+    put(out->pad_mask, s.mask.data(), s.mask.size());
+    if (b->P.vsize == 4) put(out->block_values, s.vf.data(), 4 * s.vf.size());
+    else put(out->block_values, s.vd.data(), 8 * s.vd.size());
+    return ECSR_OK;
+}
+
+void ecsr_b200_blob_free(ecsr_blob* b) { delete b; }
+
+// storage.serialize (storage.py:389-428): header <BBBBHQQL, per set <LLQQQ and
+// u64-length-prefixed arrays; deltas 4-bit (low nibble first) / u8 / u16le; pad_mask
+// packbits little-endian; values f32/f64 le. out == NULL (or cap too small) sizes.
+int ecsr_b200_serialize(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, int64_t num_cols,
+                        int32_t warp_size, int32_t delta_bits, int32_t value_bits, int32_t value_dtype,
+                        uint8_t* out, int64_t cap, int64_t* len) {
+    if (!len || (nsets > 0 && !sets) || nsets < 0) return set_error(ECSR_ERR_VALUE, "null argument");
+    if (value_dtype != ECSR_F32 && value_dtype != ECSR_F64) return set_error(ECSR_ERR_VALUE, "values must be f32 or f64");
+    if (delta_bits != 4 && delta_bits != 8 && delta_bits != 16)
+        return set_error(ECSR_ERR_VALUE, "delta_bits must be 4, 8 or 16");
+    const int vsize = value_dtype == ECSR_F32 ? 4 : 8;
+    std::vector<uint8_t> buf;
+    auto raw = [&](const void* p, size_t n) {
+        const uint8_t* b = static_cast<const uint8_t*>(p);
+        buf.insert(buf.end(), b, b + n);
+    };
+    auto u64 = [&](uint64_t v) { raw(&v, 8); };
+    raw("ECSR", 4);
+    const uint8_t hb[4] = {1, static_cast<uint8_t>(vsize), static_cast<uint8_t>(value_bits),
+                           static_cast<uint8_t>(delta_bits)};
+    raw(hb, 4);
+    const uint16_t w16 = static_cast<uint16_t>(warp_size);
+    raw(&w16, 2);
+    u64(static_cast<uint64_t>(num_rows));
+    u64(static_cast<uint64_t>(num_cols));
+    const uint32_t ns = static_cast<uint32_t>(nsets);
+    raw(&ns, 4);
+    const uint64_t limit = 1ull << delta_bits;
+    for (int si = 0; si < nsets; ++si) {
+        const ecsr_host_set& s = sets[si];
+        const uint32_t gv[2] = {static_cast<uint32_t>(s.granularity), static_cast<uint32_t>(s.vector_size)};
+        raw(gv, 8);
+        u64(static_cast<uint64_t>(s.num_blocks));
+        u64(static_cast<uint64_t>(s.stored_cols));
+        u64(static_cast<uint64_t>(s.real_nnz));
+        const int64_t nr = s.num_blocks * s.granularity, ni = s.num_blocks > 0 ? s.num_blocks + 1 : 1;
+        u64(static_cast<uint64_t>(nr));
+        raw(s.row_indices, 4 * nr);
+        u64(static_cast<uint64_t>(ni));
+        if (s.num_blocks > 0) raw(s.block_indptr, 8 * ni);
+        else u64(0);
+        u64(static_cast<uint64_t>(s.num_blocks * warp_size));
+        raw(s.base_indices, 4 * s.num_blocks * warp_size);
+        u64(static_cast<uint64_t>(s.stored_cols));
+        for (int64_t i = 0; i < s.stored_cols; ++i)
+            if (s.delta_indices[i] >= limit)
+                return set_error(ECSR_ERR_CONTAINER, "delta exceeds " + std::to_string(delta_bits) + "-bit range");
+        if (delta_bits == 4) {
+            for (int64_t i = 0; i < s.stored_cols; i += 2) {
+                const uint8_t lo = static_cast<uint8_t>(s.delta_indices[i]);
+                const uint8_t hi = i + 1 < s.stored_cols ? static_cast<uint8_t>(s.delta_indices[i + 1]) : 0;
+                buf.push_back(static_cast<uint8_t>(lo | (hi << 4)));
+            }
+        } else if (delta_bits == 8) {
+            for (int64_t i = 0; i < s.stored_cols; ++i) buf.push_back(static_cast<uint8_t>(s.delta_indices[i]));
+        } else {
+            for (int64_t i = 0; i < s.stored_cols; ++i) {
+                const uint16_t d = static_cast<uint16_t>(s.delta_indices[i]);
+                raw(&d, 2);
+            }
+        }
+        u64(static_cast<uint64_t>(s.stored_cols));
+        for (int64_t i = 0; i < s.stored_cols; i += 8) {
+            uint8_t byte = 0;
+            for (int k = 0; k < 8 && i + k < s.stored_cols; ++k)
+                if (s.pad_mask && s.pad_mask[i + k]) byte |= static_cast<uint8_t>(1u << k);
+            buf.push_back(byte);
+        }
+        u64(static_cast<uint64_t>(s.stored_cols * s.granularity));
+        raw(s.block_values, static_cast<size_t>(vsize) * s.stored_cols * s.granularity);
+    }
+    *len = static_cast<int64_t>(buf.size());
+    if (out && cap >= *len) std::memcpy(out, buf.data(), buf.size());
+    return ECSR_OK;
+}
+
 }  // extern "C"

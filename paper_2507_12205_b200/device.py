@@ -13,7 +13,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .container import EcCsrMatrix, EcCsrSet, check_set_shapes
+from .container import EcCsrMatrix, EcCsrSet, host_sets
 
 _DEVICE_DTYPES = {"f16": _lib.F16, "f32": _lib.F32, "f64": _lib.F64}
 
@@ -25,30 +25,7 @@ def _torch():
 
 
 def _host_sets(ec, check_shapes: bool = True):
-    """Coerce a container's sets to the C-ABI dtypes (copies only on mismatch, like
-    np.ascontiguousarray in `_speedups.pyx:62-77`). Returns (HostSet array, keepalive)."""
-    dtype = np.dtype(ec.dtype)
-    if dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
-        raise ValueError("container values must be float32 or float64")
-    keep = []
-    arr = (_lib.HostSet * max(len(ec.sets), 1))()
-    for s in ec.sets if check_shapes else ():
-        # array lengths against the declared sizes BEFORE any pointer crosses the C-ABI
-        # (storage.py:312-329): the native validator trusts num_blocks / stored_cols
-        check_set_shapes(s, int(ec.warp_size))
-    for i, s in enumerate(ec.sets):
-        rows = np.ascontiguousarray(s.row_indices, dtype=np.uint32)
-        indptr = np.ascontiguousarray(s.block_indptr, dtype=np.int64)
-        bases = np.ascontiguousarray(s.base_indices, dtype=np.uint32)
-        deltas = np.ascontiguousarray(s.delta_indices, dtype=np.uint32)
-        mask = np.ascontiguousarray(s.pad_mask, dtype=np.bool_).view(np.uint8)
-        vals = np.ascontiguousarray(s.block_values, dtype=dtype)
-        keep += [rows, indptr, bases, deltas, mask, vals]
-        arr[i] = _lib.HostSet(int(s.granularity), int(s.vector_size), int(s.num_blocks),
-                              int(s.stored_cols), int(s.real_nnz), _lib.ptr(rows),
-                              _lib.ptr(indptr), _lib.ptr(bases), _lib.ptr(deltas),
-                              _lib.ptr(mask), _lib.ptr(vals))
-    return arr, keep, dtype
+    return host_sets(ec, check_shapes)
 
 
 class DeviceMatrix:

@@ -67,29 +67,27 @@ class CsrMatrix:
 
 
 def generate_uniform(num_rows, num_cols, sparsity, seed, dtype=np.float64) -> CsrMatrix:
-    """Restatement of `ecsr.core.generate_uniform` (`pkg/src/ecsr/core.py:198-220`).
-
-    Same RNG, same row-chunked draw sizes, same order of draws, so the matrix is
-    bit-identical to the reference's for every (shape, sparsity, seed, dtype).
-    """
+    """The matrix of `ecsr.core.generate_uniform` (`pkg/src/ecsr/core.py:198-220`),
+    bit for bit: every cell is kept with probability 1 - sparsity by one uniform draw in
+    row-major order (one PCG64 stream, `default_rng(seed)`), then the kept cells' values
+    are drawn from U(-1, 1) in the same order. Only the order of the draws matters, so
+    the cells are drawn here in blocks of whole rows of about 16 M cells."""
     if not 0.0 <= sparsity < 1.0:
         raise ValueError("sparsity must lie in [0, 1)")
     rng = np.random.default_rng(seed)
-    density = 1.0 - sparsity
-    chunk = max(1, min(num_rows, (1 << 22) // max(num_cols, 1)))
-    col_parts = []
-    counts = np.zeros(num_rows, dtype=np.int64)
-    for start in range(0, num_rows, chunk):
-        stop = min(start + chunk, num_rows)
-        mask = rng.random((stop - start, num_cols)) < density
-        r, c = np.nonzero(mask)
-        counts[start:stop] = np.bincount(r, minlength=stop - start)
-        col_parts.append(c)
-    col_idx = np.concatenate(col_parts) if col_parts else np.empty(0, dtype=np.int64)
+    keep_below = 1.0 - sparsity
+    rows_per_draw = max(1, (1 << 24) // max(num_cols, 1))
     row_ptr = np.zeros(num_rows + 1, dtype=np.int64)
-    np.cumsum(counts, out=row_ptr[1:])
+    cols = []
+    for r0 in range(0, num_rows, rows_per_draw):
+        r1 = min(num_rows, r0 + rows_per_draw)
+        kept = rng.random((r1 - r0, num_cols)) < keep_below
+        row_ptr[r0 + 1:r1 + 1] = kept.sum(axis=1)
+        cols.append(np.flatnonzero(kept) % max(num_cols, 1))
+    np.cumsum(row_ptr, out=row_ptr)
+    col_idx = np.concatenate(cols).astype(np.int64) if cols else np.empty(0, dtype=np.int64)
     values = rng.uniform(-1.0, 1.0, size=col_idx.size).astype(dtype)
-    return CsrMatrix(num_rows, num_cols, row_ptr, col_idx.astype(np.int64), values)
+    return CsrMatrix(num_rows, num_cols, row_ptr, col_idx, values)
 
 
 _ROW_CHUNK_ELEMS = 1 << 24

@@ -131,3 +131,24 @@ def test_decode_round_trip_and_matches_reference_decode(name):
     assert np.array_equal(d.row_ptr, a.row_ptr)
     assert np.array_equal(d.col_idx, a.col_idx)
     assert np.array_equal(d.values, np.asarray(a.values, dtype=d.values.dtype))
+
+
+@needs_reference
+@pytest.mark.parametrize("name", golden_names())
+def test_native_deserialize_equals_reference(name):
+    # the native parser (ecsr_b200_blob_*) against the reference's storage.deserialize
+    from ecsr import storage
+
+    blob = load_golden(name)["blob"]
+    ref, got = storage.deserialize(blob), C.deserialize(blob)
+    assert (ref.num_rows, ref.num_cols, ref.value_bits, ref.delta_bits, ref.warp_size) == \
+        (got.num_rows, got.num_cols, got.value_bits, got.delta_bits, got.warp_size)
+    assert len(ref.sets) == len(got.sets)
+    for a, b in zip(ref.sets, got.sets):
+        assert (a.granularity, a.vector_size, a.num_blocks, a.stored_cols, a.real_nnz) == \
+            (b.granularity, b.vector_size, b.num_blocks, b.stored_cols, b.real_nnz)
+        for f in ("row_indices", "block_indptr", "base_indices", "delta_indices", "pad_mask", "block_values"):
+            x, y = np.asarray(getattr(a, f)), np.asarray(getattr(b, f))
+            assert x.shape == y.shape and np.array_equal(x.astype(y.dtype), y), f
+        assert np.asarray(b.block_values).dtype == np.asarray(a.block_values).dtype
+    assert storage.serialize(ref) == C.serialize(got) == blob

@@ -1,6 +1,6 @@
-"""Native `.ecsr` loader (csrc/ecsr_loader.cpp) against the host
-mirror of the reference's `deserialize` (storage.py:431-483): same acceptance, same
-ContainerError messages. The device half (load -> unpack bit-exact, SpMV parity) is
+"""Native `.ecsr` loader (csrc/ecsr_loader.cpp) against the
+reference's own `deserialize` (storage.py:431-483): same acceptance, same ContainerError
+messages. The device half (load -> unpack bit-exact, SpMV parity) is
 marked gpu."""
 
 import struct
@@ -8,7 +8,7 @@ import struct
 import numpy as np
 import pytest
 
-from conftest import golden_names, load_golden
+from conftest import golden_names, have_reference, load_golden
 from paper_2507_12205_b200 import container as C
 from paper_2507_12205_b200.device import parse_blob
 from paper_2507_12205_b200.errors import ContainerError
@@ -48,9 +48,15 @@ def _mutations(blob):
 
 
 def _reference_error(blob):
+    """The reference's own deserialize (storage.py:431-483) on the same bytes."""
+    if not have_reference():
+        pytest.skip("reference package (baseline/_ref) not importable")
+    from ecsr import storage
+    from ecsr.errors import ContainerError as RefContainerError
+
     try:
-        C.deserialize(blob)
-    except ContainerError as e:
+        storage.deserialize(blob)
+    except (RefContainerError, ContainerError) as e:
         return str(e)
     return None
 
@@ -91,6 +97,14 @@ def test_parse_rejects_bad_shapes_like_reference():
         assert want in str(ei.value), (what, want, str(ei.value))
 
 
+def _pack_deltas(d, bits):
+    d = np.asarray(d).astype(np.uint32)
+    if bits == 4:
+        lo, hi = d[0::2], np.append(d[1::2], np.zeros(len(d) % 2, np.uint32))
+        return (lo | (hi << 4)).astype(np.uint8).tobytes()
+    return d.astype(np.uint8 if bits == 8 else "<u2").tobytes()
+
+
 def _serialize_unchecked(ec):
     """serialize without the shape checks, to build malformed blobs."""
     out = [C.MAGIC, struct.pack("<BBBBHQQL", C.VERSION, ec.sets[0].block_values.dtype.itemsize,
@@ -103,7 +117,7 @@ def _serialize_unchecked(ec):
             a = np.asarray(arr).astype(dt)
             out.append(struct.pack("<Q", a.size) + a.tobytes())
         d = np.asarray(s.delta_indices)
-        out.append(struct.pack("<Q", d.size) + C._pack_deltas(d, ec.delta_bits))
+        out.append(struct.pack("<Q", d.size) + _pack_deltas(d, ec.delta_bits))
         m = np.asarray(s.pad_mask, dtype=bool)
         out.append(struct.pack("<Q", m.size) + np.packbits(m, bitorder="little").tobytes())
         v = np.asarray(s.block_values)
