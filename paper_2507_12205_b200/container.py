@@ -191,23 +191,26 @@ def load_container(path) -> EcCsrMatrix:
 
 
 def check_set_shapes(s, warp: int) -> None:
-    if len(s.block_indptr) != s.num_blocks + 1:
-        raise ContainerError("block_indptr length mismatch")
-    if s.block_indptr[0] != 0 or np.any(np.diff(s.block_indptr) < 0):
-        raise ContainerError("block_indptr must start at 0 and be non-decreasing")
-    if int(s.block_indptr[-1]) != s.stored_cols:
-        raise ContainerError("block_indptr does not cover stored columns")
-    if len(s.delta_indices) != s.stored_cols or len(s.pad_mask) != s.stored_cols:
-        raise ContainerError("delta or mask array length mismatch")
-    if len(s.block_values) != s.stored_cols * s.granularity:
-        raise ContainerError("block_values length mismatch")
-    if len(s.row_indices) != s.num_blocks * s.granularity:
-        raise ContainerError("row_indices length mismatch")
-    if len(s.base_indices) != s.num_blocks * warp:
-        raise ContainerError("base_indices length mismatch")
-    widths = np.diff(s.block_indptr)
-    if np.any(widths % (warp * s.vector_size)):
-        raise ContainerError("block widths must be multiples of warp_size * vector_size")
+    """Array shapes against the set's declared sizes (`storage.py:312-329`): the same
+    checks in the same order, so the same ContainerError message comes first."""
+    nb, stored, g = int(s.num_blocks), int(s.stored_cols), int(s.granularity)
+    indptr = np.asarray(s.block_indptr)
+    rules = (
+        (lambda: len(indptr) == nb + 1, "block_indptr length mismatch"),
+        (lambda: indptr[0] == 0 and not np.any(np.diff(indptr) < 0),
+         "block_indptr must start at 0 and be non-decreasing"),
+        (lambda: int(indptr[-1]) == stored, "block_indptr does not cover stored columns"),
+        (lambda: len(s.delta_indices) == stored and len(s.pad_mask) == stored,
+         "delta or mask array length mismatch"),
+        (lambda: len(s.block_values) == stored * g, "block_values length mismatch"),
+        (lambda: len(s.row_indices) == nb * g, "row_indices length mismatch"),
+        (lambda: len(s.base_indices) == nb * warp, "base_indices length mismatch"),
+        (lambda: not np.any(np.diff(indptr) % (warp * int(s.vector_size))),
+         "block widths must be multiples of warp_size * vector_size"),
+    )
+    for ok, message in rules:
+        if not ok():
+            raise ContainerError(message)
 
 
 def lane_tops(s, warp: int) -> np.ndarray:
