@@ -159,7 +159,7 @@ void ecsr_b200_group_free(ecsr_group* group);
  * waits until every peer's push into this rank landed -- the NCCL all-gather + index
  * assembly of the sharded step in one launch. Setup: create (y_full bytes, rank,
  * world <= 16), export handle (64 B) -> all-gather the handles (host) -> open, plan the
- * segments once (src/dst byte offsets, multiples of 4). ecsr_b200_xchg_y: the local
+ * segments once (<= 64; src/dst byte offsets, multiples of 4). ecsr_b200_xchg_y: the local
  * y_full. Steps are counted on the device, so the run can be graph-captured. */
 typedef struct ecsr_xchg ecsr_xchg;
 typedef struct ecsr_xchg_seg {

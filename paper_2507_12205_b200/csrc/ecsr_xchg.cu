@@ -35,11 +35,12 @@ int set_error(int code, const std::string& msg);
 namespace {
 
 constexpr int kMaxRanks = 16;
+constexpr int kMaxSegs = 64;  // segments ride in the kernel parameters (no dependent loads)
 constexpr int kLine = 128;
 
 struct XchgParams {
     const uint8_t* src;                 // this rank's SpMV output (device)
-    const ecsr_xchg_seg* segs;          // [nsegs] (device)
+    ecsr_xchg_seg segs[kMaxSegs];
     int32_t nsegs;
     int32_t rank, world;
     int32_t parts;                      // CTAs per destination rank
@@ -117,15 +118,13 @@ struct ecsr_xchg {
     uint8_t* buf = nullptr;                     // own buffer
     std::vector<uint8_t*> peer;                 // mapped peer buffers (own at [rank])
     std::vector<bool> opened;                   // cudaIpcOpenMemHandle'd (to close)
-    ecsr_xchg_seg* d_segs = nullptr;            // device copy of the segment table
-    int32_t nsegs = 0;
+    std::vector<ecsr_xchg_seg> segs;            // the planned segments
     ~ecsr_xchg() {
         int prev = -1;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         for (size_t i = 0; i < peer.size(); ++i)
             if (opened[i] && peer[i]) cudaIpcCloseMemHandle(peer[i]);
-        if (d_segs) cudaFree(d_segs);
         if (buf) cudaFree(buf);
         if (prev >= 0) cudaSetDevice(prev);
     }
@@ -188,30 +187,23 @@ void* ecsr_b200_xchg_y(const ecsr_xchg* x) { return x ? x->buf : nullptr; }
 
 int ecsr_b200_xchg_plan(ecsr_xchg* x, const ecsr_xchg_seg* segs, int32_t nsegs) {
     if (!x || (!segs && nsegs > 0) || nsegs < 0) return fail(ECSR_ERR_VALUE, "null argument");
+    if (nsegs > kMaxSegs) return fail(ECSR_ERR_VALUE, "at most " + std::to_string(kMaxSegs) + " segments");
     for (int i = 0; i < nsegs; ++i)
         if (segs[i].src_off < 0 || segs[i].bytes < 0 || (segs[i].bytes & 3) || (segs[i].src_off & 3) ||
             (segs[i].dst_off & 3) || segs[i].dst_off < 0 || segs[i].dst_off + segs[i].bytes > x->y_bytes)
             return fail(ECSR_ERR_VALUE, "segment outside y_full or not 4-byte aligned");
-    if (x->d_segs) cudaFree(x->d_segs);
-    x->d_segs = nullptr;
-    x->nsegs = 0;
-    if (nsegs) {
-        cudaError_t e = cudaMalloc(&x->d_segs, sizeof(ecsr_xchg_seg) * nsegs);
-        if (e == cudaSuccess) e = cudaMemcpy(x->d_segs, segs, sizeof(ecsr_xchg_seg) * nsegs, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return fail(ECSR_ERR_CUDA, std::string("xchg segments: ") + cudaGetErrorString(e));
-    }
-    x->nsegs = nsegs;
+    x->segs.assign(segs, segs + nsegs);
     return ECSR_OK;
 }
 
 int ecsr_b200_xchg_run(const ecsr_xchg* x, const void* src, void* stream) {
-    if (!x || (!src && x->nsegs > 0)) return fail(ECSR_ERR_VALUE, "null argument");
+    if (!x || (!src && !x->segs.empty())) return fail(ECSR_ERR_VALUE, "null argument");
     for (int r = 0; r < x->world; ++r)
         if (!x->peer[r]) return fail(ECSR_ERR_VALUE, "peer buffers not opened (ecsr_b200_xchg_open)");
     XchgParams p{};
     p.src = static_cast<const uint8_t*>(src);
-    p.segs = x->d_segs;
-    p.nsegs = x->nsegs;
+    for (size_t i = 0; i < x->segs.size(); ++i) p.segs[i] = x->segs[i];
+    p.nsegs = static_cast<int32_t>(x->segs.size());
     p.rank = x->rank;
     p.world = x->world;
     p.parts = std::max(1, 32 / x->world);  // >= 32 CTAs push, each destination gets 32/world

@@ -49,8 +49,8 @@ def run(env):
 run({})
 for env in [{"ECSR_B200_TILE": 11000, "ECSR_B200_RECCAP": 8600, "ECSR_B200_RECMAX": 11000},
             {"ECSR_B200_TILE": 13000, "ECSR_B200_RECCAP": 8600, "ECSR_B200_RECMAX": 13000},
-            {"ECSR_B200_TILE": 11000, "ECSR_B200_RECCAP": 11000, "ECSR_B200_RECMAX": 11000},
-            {"ECSR_B200_TILE": 13000, "ECSR_B200_RECCAP": 6500, "ECSR_B200_RECMAX": 13000},
-            {"ECSR_B200_RECMAX": 17000}]:
+            {"ECSR_B200_TILE": 8600, "ECSR_B200_RECCAP": 8600, "ECSR_B200_RECMAX": 8600},
+            {"ECSR_B200_TILE": 12500, "ECSR_B200_RECCAP": 6000, "ECSR_B200_RECMAX": 12500},
+            {"ECSR_B200_TILE": 20500}]:
     run(env)
 run({})
