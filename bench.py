@@ -749,13 +749,16 @@ def run_ours(args):
         launch_ms[ln] = tot / n
 
     # end-to-end through the public API: every step copies ALL of its inputs in (pinned
-    # host x -> device) and ALL of its outputs out (device y -> pinned host) around its
-    # grouped launch. Steps are pipelined over two device buffer sets on a copy stream:
-    # step i's x goes up while step i-1 computes, and step i-1's y comes down while step
-    # i computes; the timed region is whole graphs of `spg` such steps.
+    # host x -> device) and ALL of its outputs out (device y -> pinned host). The copies
+    # are host-io kernels in the launch chain (device.host_io, csrc/ecsr_hostio.cu), not
+    # copy-stream memcpys: a launch waiting on a copy node loses its PDL edge (+5 us per
+    # step, scripts/e2e_probe.py). io(i) moves x(i) in and y(i-2) out while launch i-1
+    # runs (two device buffer sets); after the last launch, y(n-2) and then y(n-1). The
+    # timed region is whole graphs of `spg` such steps.
+    from paper_2507_12205_b200.device import host_io
+
     h2d = sum(x.numel() * 2 for x in wl.xs_host.values())
     d2h = sum(y.numel() * 4 for y in wl.ys_host.values())
-    copy = torch.cuda.Stream(dev)
     x_dev = [wl.x_all, torch.empty_like(wl.x_all)]
     y_dev = [wl.y_all, torch.empty_like(wl.y_all)]
     y_host = [wl.y_host_all, torch.empty_like(wl.y_host_all).pin_memory()]
@@ -771,34 +774,17 @@ def run_ours(args):
     y_lists = [views(y, wl.y_list) for y in y_dev]
 
     def e2e_steps(n):
-        start = torch.cuda.Event()
-        start.record(stream)
-        copy.wait_event(start)
-        x_in, k_done = [], []
-        with torch.cuda.stream(copy):
-            for i in range(min(2, n)):
-                x_dev[i % 2].copy_(wl.x_host_all, non_blocking=True)
-                e = torch.cuda.Event()
-                e.record(copy)
-                x_in.append(e)
         for i in range(n):
             b = i % 2
-            stream.wait_event(x_in[i])
+            # x_host_all / y_host_all hold exactly the step's x and y (16-B padded slices)
+            pairs = [(wl.x_host_all, x_dev[b])]
+            if i >= 2:  # y(i-2) sits in y_dev[b]; launch i overwrites it only after io(i)
+                pairs.append((y_dev[b], y_host[b]))
+            host_io(pairs, stream)
             wl.group.spmv(x_lists[b], y_lists[b], stream=stream)
-            e = torch.cuda.Event()
-            e.record(stream)
-            k_done.append(e)
-            with torch.cuda.stream(copy):
-                copy.wait_event(k_done[i])
-                y_host[b].copy_(y_dev[b], non_blocking=True)
-                if i + 2 < n:  # after step i's y left buffer b, step i+2's x may enter it
-                    x_dev[b].copy_(wl.x_host_all, non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(copy)
-                    x_in.append(e)
-        done = torch.cuda.Event()
-        done.record(copy)
-        stream.wait_event(done)  # join
+        if n >= 2:
+            host_io([(y_dev[(n - 2) % 2], y_host[(n - 2) % 2])], stream)
+        host_io([(y_dev[(n - 1) % 2], y_host[(n - 1) % 2])], stream, after_predecessor=True)
 
     with torch.cuda.stream(stream):
         e2e_steps(2)
@@ -838,8 +824,10 @@ def run_ours(args):
         "e2e": {"value": round(wl.step_bytes / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps_per_graph": spg,
-                "note": "every step: pinned-host x -> device, grouped launch, device y -> pinned host; "
-                        "copies pipelined with the neighbouring steps' launches (two buffer sets)"},
+                "launches_per_step": 2, "io": "ecsr_b200_host_io",
+                "note": "every step: pinned-host x -> device and device y -> pinned host (all of the "
+                        "step's inputs and outputs) by a host-io kernel chained in front of the grouped "
+                        "launch, overlapping the previous launch (two device buffer sets)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": wl.step_bytes,

@@ -174,6 +174,22 @@ int ecsr_b200_xchg_plan(ecsr_xchg* xchg, const ecsr_xchg_seg* segs, int32_t nseg
 int ecsr_b200_xchg_run(const ecsr_xchg* xchg, const void* src, void* stream);
 void* ecsr_b200_xchg_y(const ecsr_xchg* xchg);
 void ecsr_b200_xchg_free(ecsr_xchg* xchg);
+/* A step's host traffic as one PDL-chained kernel (end-to-end leg):
+ * copies each span (src -> dst; device memory of the current device or pinned host
+ * memory, which the GPU reaches through its UVA mapping; 16-B aligned, bytes a multiple
+ * of 16) with plain loads/stores, in the stream's launch chain instead of on a copy
+ * stream, so the next SpMV keeps its programmatic edge (csrc/ecsr_hostio.cu). Default:
+ * the copies overlap the preceding launch and the kernel completes after it (the spans
+ * must not be written by that launch); ECSR_IO_AFTER_PREDECESSOR: wait for it first
+ * (read a result the preceding launch wrote). */
+#define ECSR_IO_MAX_SPANS 16
+#define ECSR_IO_AFTER_PREDECESSOR 1
+typedef struct ecsr_io_span {
+    const void* src;
+    void* dst;
+    int64_t bytes;
+} ecsr_io_span;
+int ecsr_b200_host_io(const ecsr_io_span* spans, int32_t nspans, int32_t flags, void* stream);
 /* .ecsr wire format (storage.py:389-483) straight to a device handle, no numpy round trip
  * (SURVEY.md §8(f) #3). ecsr_b200_parse parses and shape-checks a blob on the host only,
  * rejecting corruption with the reference's ContainerError (code 1) and message: bad

@@ -21,6 +21,7 @@ OK, ERR_CONTAINER, ERR_VALUE, ERR_CUDA = 0, 1, 2, 3
 F16, F32, F64 = 1, 2, 3
 PACK_DEFAULT, PACK_FORCE_GENERIC = 0, 1
 SPMV_OVERWRITE, SPMV_ACCUMULATE, SPMV_ORDERED, SPMV_MEMSET_Y = 0, 1, 2, 4
+IO_AFTER_PREDECESSOR = 1  # include/ecsr_b200.h ECSR_IO_AFTER_PREDECESSOR
 
 _DTYPE_CODE = {np.dtype(np.float16): F16, np.dtype(np.float32): F32, np.dtype(np.float64): F64}
 
@@ -99,6 +100,7 @@ SIGNATURES = {
     "ecsr_b200_xchg_run": (c_i32, [c_vp, c_vp, c_vp]),
     "ecsr_b200_xchg_y": (c_vp, [c_vp]),
     "ecsr_b200_xchg_free": (None, [c_vp]),
+    "ecsr_b200_host_io": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
     "ecsr_b200_trace": (c_i32, [c_vp, c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "ecsr_b200_spmv_set": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_i64, c_i32]),

@@ -271,6 +271,36 @@ class SpmvGroup:
         return outs
 
 
+class _IoSpan(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("bytes", ctypes.c_int64)]
+
+
+def host_io(pairs, stream=None, after_predecessor: bool = False) -> None:
+    """A step's host traffic as one kernel in the stream's launch chain
+    (`ecsr_b200_host_io`, csrc/ecsr_hostio.cu): copies every (src, dst) tensor pair --
+    CUDA tensors of the current device or pinned host tensors, same byte size, 16-B
+    aligned, contiguous -- without a copy stream, so the next SpMV keeps its PDL edge.
+    The copies overlap the preceding launch unless `after_predecessor` (then they read
+    what it wrote); the caller keeps the preceding launch off the spans."""
+    torch = _torch()
+    spans = []
+    for src, dst in pairs:
+        for t in (src, dst):
+            if not isinstance(t, torch.Tensor) or not t.is_contiguous():
+                raise ValueError("host_io: contiguous tensors required")
+            if not t.is_cuda and not t.is_pinned():
+                raise ValueError("host_io: host tensors must be pinned")
+        nb = src.numel() * src.element_size()
+        if nb != dst.numel() * dst.element_size():
+            raise ValueError(f"host_io: src has {nb} bytes, dst {dst.numel() * dst.element_size()}")
+        spans.append(_IoSpan(src.data_ptr(), dst.data_ptr(), nb))
+    dev = next((t.device for p in pairs for t in p if t.is_cuda), None)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    arr = (_IoSpan * max(1, len(spans)))(*spans)
+    _lib.check(_lib.lib().ecsr_b200_host_io(arr, len(spans), _lib.IO_AFTER_PREDECESSOR if after_predecessor else 0,
+                                            ctypes.c_void_p(s.cuda_stream)), "ecsr_b200_host_io")
+
+
 def spmv_host(W: DeviceMatrix, x: np.ndarray, ordered: bool = False) -> np.ndarray:
     """End-to-end call with host buffers: H2D x, SpMV, D2H y (synchronous)."""
     torch = _torch()

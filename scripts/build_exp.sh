@@ -6,5 +6,5 @@ set -e
 name=$1; shift
 mkdir -p build
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2,-fopenmp,-mpopcnt "$@" \
-  -shared -o build/lib$name.so paper_2507_12205_b200/csrc/ecsr_b200.cu paper_2507_12205_b200/csrc/ecsr_xchg.cu \
+  -shared -o build/lib$name.so paper_2507_12205_b200/csrc/ecsr_b200.cu paper_2507_12205_b200/csrc/ecsr_xchg.cu paper_2507_12205_b200/csrc/ecsr_hostio.cu \
   paper_2507_12205_b200/csrc/ecsr_encoder.cpp paper_2507_12205_b200/csrc/ecsr_loader.cpp -lgomp
