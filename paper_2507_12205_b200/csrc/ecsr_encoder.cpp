@@ -24,6 +24,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -74,70 +75,167 @@ struct Cfg {
 };
 
 // --- row_matching (extraction.py:153-178) -------------------------------------------
-std::vector<std::pair<int64_t, int64_t>> row_matching(const Level& L, int64_t K, const Cfg& cfg) {
+// Rounds of one level re-match every row, but a round only changes the rows it paired
+// (their shared columns leave). MatchCache keeps, per level, the candidates' column
+// bitsets and their pairwise overlaps (upper triangle, uint16: overlaps <= K < 65536);
+// a round recomputes only the rows the previous one changed. Without room for the
+// triangle (or K >= 65536) every overlap is computed on the fly, pruned by the nnz bound.
+constexpr int64_t kMaxCacheBytes = int64_t{1} << 30;
+
+struct MatchCache {
+    bool built = false, tri_ok = false;
+    int64_t words = 0;
+    std::vector<int64_t> cand, cidx;  // candidate rows (nnz >= bar when built), inverse map
+    std::vector<uint64_t> bits;       // cand x words
+    std::vector<uint16_t> tri;        // overlap(c1 < c2) at tidx(c1, c2)
+    std::vector<int64_t> dirty;       // rows changed since the cache was brought up to date
+    int64_t tidx(int64_t a, int64_t b) const {  // a < b
+        const int64_t n = static_cast<int64_t>(cand.size());
+        return a * n - a * (a + 1) / 2 + (b - a - 1);
+    }
+};
+
+int64_t popand(const uint64_t* a, const uint64_t* b, int64_t words) {
+    int64_t cnt = 0;
+    for (int64_t w = 0; w < words; ++w) cnt += __builtin_popcountll(a[w] & b[w]);
+    return cnt;
+}
+
+void set_bits(const Level& L, int64_t r, uint64_t* b, int64_t words) {
+    std::memset(b, 0, words * sizeof(uint64_t));
+    for (int64_t p = L.row_ptr[r]; p < L.row_ptr[r + 1]; ++p) b[L.col[p] >> 6] |= uint64_t{1} << (L.col[p] & 63);
+}
+
+void refresh_cache(const Level& L, int64_t K, int64_t bar, MatchCache* mc) {
     const int64_t M = L.rows;
-    const int64_t words = (K + 63) / 64;
+    if (!mc->built) {
+        mc->words = (K + 63) / 64;
+        mc->cand.clear();
+        for (int64_t r = 0; r < M; ++r)
+            if (L.row_ptr[r + 1] - L.row_ptr[r] >= bar) mc->cand.push_back(r);
+        const int64_t nc = static_cast<int64_t>(mc->cand.size());
+        mc->cidx.assign(M, -1);
+        for (int64_t c = 0; c < nc; ++c) mc->cidx[mc->cand[c]] = c;
+        mc->bits.assign(nc * mc->words, 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < nc; ++c) set_bits(L, mc->cand[c], mc->bits.data() + c * mc->words, mc->words);
+        mc->tri_ok = K < 65536 && nc * (nc - 1) / 2 * 2 <= kMaxCacheBytes;
+        if (mc->tri_ok) {
+            mc->tri.assign(nc * (nc - 1) / 2, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+            for (int64_t a = 0; a < nc; ++a) {
+                const uint64_t* ba = mc->bits.data() + a * mc->words;
+                uint16_t* out = mc->tri.data() + mc->tidx(a, a + 1);
+                for (int64_t b = a + 1; b < nc; ++b)
+                    out[b - a - 1] = static_cast<uint16_t>(popand(ba, mc->bits.data() + b * mc->words, mc->words));
+            }
+        }
+        mc->built = true;
+        mc->dirty.clear();
+        return;
+    }
+    // rows changed by the last round: new bitsets, then their overlaps with every candidate
+    std::vector<int64_t> dc;
+    for (int64_t r : mc->dirty)
+        if (mc->cidx[r] >= 0) dc.push_back(mc->cidx[r]);
+    std::sort(dc.begin(), dc.end());
+    dc.erase(std::unique(dc.begin(), dc.end()), dc.end());
+    mc->dirty.clear();
+    const int64_t nd = static_cast<int64_t>(dc.size());
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < nd; ++k) set_bits(L, mc->cand[dc[k]], mc->bits.data() + dc[k] * mc->words, mc->words);
+    if (!mc->tri_ok || nd == 0) return;
+    const int64_t nc = static_cast<int64_t>(mc->cand.size());
+    std::vector<uint8_t> isd(nc, 0);
+    for (int64_t c : dc) isd[c] = 1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t k = 0; k < nd; ++k) {
+        const int64_t d = dc[k];
+        const uint64_t* bd = mc->bits.data() + d * mc->words;
+        for (int64_t c = 0; c < nc; ++c) {
+            if (c == d || (isd[c] && c < d)) continue;  // a pair of changed rows: the smaller writes
+            const uint16_t v = static_cast<uint16_t>(popand(bd, mc->bits.data() + c * mc->words, mc->words));
+            mc->tri[c < d ? mc->tidx(c, d) : mc->tidx(d, c)] = v;
+        }
+    }
+}
+
+std::vector<std::pair<int64_t, int64_t>> row_matching(const Level& L, int64_t K, const Cfg& cfg, MatchCache* mc) {
+    const int64_t M = L.rows;
     const int64_t bar = cfg.chunk();
+    refresh_cache(L, K, bar, mc);
+    const int64_t words = mc->words;
     std::vector<int64_t> nnz(M);
     for (int64_t r = 0; r < M; ++r) nnz[r] = L.row_ptr[r + 1] - L.row_ptr[r];
-    // only rows that can reach the bar are ever chosen as partners
-    std::vector<int64_t> cand;
-    for (int64_t r = 0; r < M; ++r)
-        if (nnz[r] >= bar) cand.push_back(r);
-    std::vector<int64_t> cidx(M, -1);
-    for (size_t c = 0; c < cand.size(); ++c) cidx[cand[c]] = static_cast<int64_t>(c);
-    std::vector<uint64_t> bits(cand.size() * words, 0);
-#pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < static_cast<int64_t>(cand.size()); ++c) {
-        const int64_t r = cand[c];
-        uint64_t* b = bits.data() + c * words;
-        for (int64_t p = L.row_ptr[r]; p < L.row_ptr[r + 1]; ++p) b[L.col[p] >> 6] |= uint64_t{1} << (L.col[p] & 63);
-    }
+    // only rows that can reach the bar are ever chosen as partners (nnz only shrinks
+    // within a level, so the candidates of the cache's first round cover them)
+    const std::vector<int64_t>& cand = mc->cand;
+    const std::vector<int64_t>& cidx = mc->cidx;
+    const int64_t nc = static_cast<int64_t>(cand.size());
     std::vector<uint8_t> avail(M, 0);
     for (int64_t r = 0; r < M; ++r) avail[r] = nnz[r] > 0;
-    std::vector<uint8_t> cavail(cand.size(), 1);
+    std::vector<uint8_t> cavail(nc, 1);
     std::vector<std::pair<int64_t, int64_t>> pairs;
     const int nth = omp_get_max_threads();
-    std::vector<int64_t> tbest(nth), tidx(nth);
-    for (int64_t i = 0; i < M; ++i) {
-        if (!avail[i]) continue;  // empty rows are never visited; taken rows are skipped
-        avail[i] = 0;
-        if (cidx[i] >= 0) cavail[cidx[i]] = 0;
-        if (nnz[i] < bar) continue;  // its best overlap is below the bar: stays unmatched
-        const uint64_t* bi = bits.data() + cidx[i] * words;
-        const int64_t c0 = cidx[i] + 1;  // available candidates all lie above row i
-        const int64_t nc = static_cast<int64_t>(cand.size());
+    std::vector<int64_t> tbest(nth, -1), tidx(nth, -1);
+    // A candidate sharing ALL of row i's columns cannot be beaten, and ties go to the
+    // smaller row: once one is found, no candidate above it can be chosen (planted blocks
+    // make such rows common).
+    std::atomic<int64_t> full_at{nc};
+    // One parallel region for the whole greedy pass: every thread walks the rows in
+    // order and scans its index range of row i's candidates; one thread then takes the
+    // argmax and marks the partner (a row is visited once, and only candidates above it
+    // are scanned, so nothing else needs updating).
 #pragma omp parallel num_threads(nth)
-        {
-            const int t = omp_get_thread_num();
+    {
+        const int t = omp_get_thread_num();
+        const int nt = omp_get_num_threads();
+        for (int64_t i = 0; i < M; ++i) {
+            // empty rows are never visited; taken rows are skipped; a row below the bar
+            // stays unmatched (its best overlap is below it)
+            if (!avail[i] || nnz[i] < bar) continue;
+            const int64_t ci = cidx[i];
+            const uint64_t* bi = mc->bits.data() + ci * words;
+            const uint16_t* trow = mc->tri_ok ? mc->tri.data() + mc->tidx(ci, ci + 1) - (ci + 1) : nullptr;
+            const int64_t c0 = ci + 1;  // available candidates all lie above row i
+            const int64_t per = (nc - c0 + nt - 1) / nt;  // thread t: the t-th index range
+            const int64_t lo = c0 + t * per, hi = std::min(nc, lo + per);
             int64_t best = -1, bidx = -1;
-#pragma omp for schedule(static) nowait
-            for (int64_t c = c0; c < nc; ++c) {
+            for (int64_t c = lo; c < hi; ++c) {
+                if (c > full_at.load(std::memory_order_relaxed)) break;
                 if (!cavail[c]) continue;
                 const int64_t up = std::min(nnz[i], nnz[cand[c]]);
                 if (up < bar || up <= best) continue;  // cannot win (ties keep the smaller row)
-                const uint64_t* bj = bits.data() + c * words;
-                int64_t cnt = 0;
-                for (int64_t w = 0; w < words; ++w) cnt += __builtin_popcountll(bi[w] & bj[w]);
+                const int64_t cnt = trow ? static_cast<int64_t>(trow[c]) : popand(bi, mc->bits.data() + c * words, words);
                 if (cnt > best) {
                     best = cnt;
                     bidx = c;
+                    if (cnt == nnz[i]) {
+                        int64_t cur = full_at.load(std::memory_order_relaxed);
+                        while (c < cur && !full_at.compare_exchange_weak(cur, c, std::memory_order_relaxed)) {
+                        }
+                        break;
+                    }
                 }
             }
             tbest[t] = best;
             tidx[t] = bidx;
-        }
-        int64_t best = -1, bidx = -1;
-        for (int t = 0; t < nth; ++t)  // static schedule: thread t holds a lower index range
-            if (tbest[t] > best) {
-                best = tbest[t];
-                bidx = tidx[t];
-            }
-        if (best >= bar) {
-            const int64_t j = cand[bidx];
-            pairs.emplace_back(i, j);
-            avail[j] = 0;
-            cavail[bidx] = 0;
+#pragma omp barrier
+#pragma omp single
+            {
+                int64_t b = -1, bx = -1;
+                for (int k = 0; k < nt; ++k)  // thread k holds a lower index range than k + 1
+                    if (tbest[k] > b) {
+                        b = tbest[k];
+                        bx = tidx[k];
+                    }
+                if (b >= bar) {
+                    pairs.emplace_back(i, cand[bx]);
+                    avail[cand[bx]] = 0;
+                    cavail[bx] = 0;
+                }
+                full_at.store(nc, std::memory_order_relaxed);
+            }  // implicit barrier: every thread sees the update before row i + 1
         }
     }
     return pairs;
@@ -151,17 +249,20 @@ struct Unit {
 };
 
 bool extract_round(Level& L, const std::vector<std::pair<int64_t, int64_t>>& pairs, const Cfg& cfg,
-                   std::vector<Unit>* units) {
+                   std::vector<Unit>* units, std::vector<int64_t>* changed) {
     const int g = L.g();
     const int64_t nnz = L.row_ptr[L.rows];
     std::vector<uint8_t> keep(nnz, 1);
-    size_t before = units->size();
-    std::vector<int32_t> shared;
-    std::vector<int64_t> pi, pj;
-    for (auto [i, j] : pairs) {
-        shared.clear();
-        pi.clear();
-        pj.clear();
+    const int64_t np = static_cast<int64_t>(pairs.size());
+    std::vector<Unit> made(np);
+    std::vector<uint8_t> has(np, 0);
+    // the pairs of a matching are disjoint rows: each one's intersection and its `keep`
+    // marks are independent of the others'
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t q = 0; q < np; ++q) {
+        const int64_t i = pairs[q].first, j = pairs[q].second;
+        std::vector<int32_t> shared;
+        std::vector<int64_t> pi, pj;
         int64_t a = L.row_ptr[i], ae = L.row_ptr[i + 1], b = L.row_ptr[j], be = L.row_ptr[j + 1];
         while (a < ae && b < be) {  // np.intersect1d(assume_unique, return_indices)
             if (L.col[a] < L.col[b]) ++a;
@@ -186,7 +287,8 @@ bool extract_round(Level& L, const std::vector<std::pair<int64_t, int64_t>>& pai
             s = e;
         }
         if (take.empty()) continue;
-        Unit u;
+        Unit& u = made[q];
+        has[q] = 1;
         u.cols.reserve(take.size());
         u.payload.reserve(take.size() * 2 * g);
         for (int64_t k : take) {
@@ -200,7 +302,15 @@ bool extract_round(Level& L, const std::vector<std::pair<int64_t, int64_t>>& pai
         }
         u.row_ids.insert(u.row_ids.end(), L.row_map.begin() + i * g, L.row_map.begin() + (i + 1) * g);
         u.row_ids.insert(u.row_ids.end(), L.row_map.begin() + j * g, L.row_map.begin() + (j + 1) * g);
-        units->push_back(std::move(u));
+    }
+    size_t before = units->size();
+    for (int64_t q = 0; q < np; ++q) {  // units in the matching's order
+        if (!has[q]) continue;
+        if (changed) {
+            changed->push_back(pairs[q].first);
+            changed->push_back(pairs[q].second);
+        }
+        units->push_back(std::move(made[q]));
     }
     if (units->size() == before) return false;
     // _filter_entries (extraction.py:202-215)
@@ -209,18 +319,25 @@ bool extract_round(Level& L, const std::vector<std::pair<int64_t, int64_t>>& pai
     R.rows = L.rows;
     R.row_map = std::move(L.row_map);
     R.row_ptr.assign(L.rows + 1, 0);
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < L.rows; ++r) {
         int64_t c = 0;
         for (int64_t p = L.row_ptr[r]; p < L.row_ptr[r + 1]; ++p) c += keep[p];
-        R.row_ptr[r + 1] = R.row_ptr[r] + c;
+        R.row_ptr[r + 1] = c;
     }
-    R.col.reserve(R.row_ptr[L.rows]);
-    R.payload.reserve(R.row_ptr[L.rows] * g);
-    for (int64_t p = 0; p < nnz; ++p)
-        if (keep[p]) {
-            R.col.push_back(L.col[p]);
-            R.payload.insert(R.payload.end(), L.payload.begin() + p * g, L.payload.begin() + (p + 1) * g);
-        }
+    for (int64_t r = 0; r < L.rows; ++r) R.row_ptr[r + 1] += R.row_ptr[r];
+    R.col.resize(R.row_ptr[L.rows]);
+    R.payload.resize(R.row_ptr[L.rows] * g);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < L.rows; ++r) {
+        int64_t o = R.row_ptr[r];
+        for (int64_t p = L.row_ptr[r]; p < L.row_ptr[r + 1]; ++p)
+            if (keep[p]) {
+                R.col[o] = L.col[p];
+                std::memcpy(R.payload.data() + o * g, L.payload.data() + p * g, g * sizeof(double));
+                ++o;
+            }
+    }
     L = std::move(R);
     return true;
 }
@@ -297,9 +414,10 @@ std::vector<BlockSet> extract_blocks(Level enc, int64_t K, const Cfg& cfg) {
             break;
         }
         std::vector<Unit> units;
+        MatchCache cache;  // this level's rows
         while (true) {  // multi_round_extract
-            auto pairs = row_matching(enc, K, cfg);
-            if (!extract_round(enc, pairs, cfg, &units)) break;
+            auto pairs = row_matching(enc, K, cfg, &cache);
+            if (!extract_round(enc, pairs, cfg, &units, &cache.dirty)) break;
         }
         sets.push_back(decode_residual(enc, cfg));
         if (units.empty()) break;
