@@ -103,7 +103,6 @@ WORKLOADS = {
     },
     "llama2-13b-layer-planted-s0.5": {
         "desc": "LLaMA-2-13B decoder layer, planted multi-granularity blocks @50 % (BASELINE configs[2])",
-        "opt_in": True,  # ~1-2 min of native encoding on the box: --all-configs
         "matrices": [
             ("q", "planted", 5120, 5120, 0.5, 31), ("k", "planted", 5120, 5120, 0.5, 302),
             ("v", "planted", 5120, 5120, 0.5, 303), ("o", "planted", 5120, 5120, 0.5, 304),
@@ -865,8 +864,7 @@ def run_ours(args):
     del wl, graph, graph_c, g_e2e, x_dev, y_dev, y_host, x_lists, y_lists
     torch.cuda.synchronize()
     if not args.no_extra:
-        line["configs"] = [bench_extra(n, dev, stream, args, peak) for n in WORKLOADS
-                           if n != HEADLINE and (args.all_configs or not WORKLOADS[n].get("opt_in"))]
+        line["configs"] = [bench_extra(n, dev, stream, args, peak) for n in WORKLOADS if n != HEADLINE]
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(mbytes, budget_s=args.cpu_budget)
     line["native_so_loaded"] = loaded_native_libs()
@@ -1170,8 +1168,6 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
-    ap.add_argument("--all-configs", action="store_true",
-                    help="also time the opt-in configs (the LLaMA-2-13B planted layer)")
     ap.add_argument("--shard", action="store_true", help="use the row-sharded path even at N=1")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="sharded y exchange: NVLink peer stores (one kernel) or NCCL all-gather")

@@ -6,7 +6,8 @@ tiled kernel: small containers, every launch mode, checked against the oracle.
 Covers: the smoke container (one tile per CTA), a 1024x4096 matrix packed with 1 KB
 tiles (many tiles per CTA: the stage pool, the tile->stage map and the tail queue
 wrap), the u32-base (K > 65535) variant, two streams sharing one handle, overwrite /
-accumulate / ordered modes, and a grouped launch (gated and memset overwrite)."""
+accumulate / ordered modes, a grouped launch (gated and memset overwrite), and the
+host-io chain around it (ecsr_b200_host_io)."""
 import os
 import sys
 
@@ -82,4 +83,31 @@ for memset_y in (False, True, False):
         err = np.max(np.abs(y.cpu().numpy() - r)) / max(np.max(np.abs(r)), 1e-30)
         assert err <= 1e-5, ("group", err)
 print("group of 3: ok", flush=True)
+# host-io chain: io(i) stages x(i) (pinned host -> device) and writes y(i-2) out while
+# the previous grouped launch runs; the last two y after the last launch
+from paper_2507_12205_b200.device import host_io  # noqa: E402
+
+n = 4
+xh = [torch.cat([torch.from_numpy(np.random.default_rng(20 + i).uniform(-1, 1, e.num_cols).astype(np.float16))
+                 for e in ecs]).pin_memory() for i in range(n)]
+kx = [e.num_cols for e in ecs]
+xdev = [torch.zeros_like(xh[0], device="cuda") for _ in range(2)]
+ydev = [torch.zeros(sum(e.num_rows for e in ecs), device="cuda") for _ in range(2)]
+yh = [torch.zeros(ydev[0].numel()).pin_memory() for _ in range(n)]
+xv = [list(torch.split(xdev[b], kx)) for b in range(2)]
+yv = [list(torch.split(ydev[b], [e.num_rows for e in ecs])) for b in range(2)]
+for i in range(n):
+    b = i % 2
+    host_io([(xh[i], xdev[b])] + ([(ydev[b], yh[i - 2])] if i >= 2 else []))
+    g.spmv(xv[b], yv[b])
+host_io([(ydev[(n - 2) % 2], yh[n - 2])])
+host_io([(ydev[(n - 1) % 2], yh[n - 1])], after_predecessor=True)
+torch.cuda.synchronize()
+for i in range(n):
+    got = torch.split(yh[i], [e.num_rows for e in ecs])
+    for e, xs_i, y in zip(ecs, torch.split(xh[i], kx), got):
+        r = ref16(e, xs_i.numpy().astype(np.float64))
+        err = np.max(np.abs(y.numpy() - r)) / max(np.max(np.abs(r)), 1e-30)
+        assert err <= 1e-5, ("host io", i, err)
+print("host-io chain of 4: ok", flush=True)
 print("sanitize workload done")
