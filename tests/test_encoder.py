@@ -41,6 +41,8 @@ def test_native_encoder_matches_reference_golden(name):
     ("planted", 384, 384, 0.5, 12, 32, 4, 8, 200, None),
     ("planted", 384, 384, 0.5, 13, 32, 4, 8, None, 1),
     ("uniform", 64, 1024, 0.97, 14, 32, 4, 4, None, None),
+    # K >= 65536: overlaps exceed the uint16 cache, the matching computes them on the fly
+    ("planted", 128, 66000, 0.9, 15, 32, 4, 8, None, None),
 ])
 def test_native_encoder_matches_live_reference(kind, m, k, s, seed, w, v, b, clip, levels):
     from ecsr import core, storage
