@@ -61,7 +61,9 @@ bool coop_launch() { return env_int("ECSR_B200_COOP", 0) != 0; }
 bool group_force_cps1() { return env_int("ECSR_B200_GROUP_CPS1", 0) != 0; }
 bool pack_ffd() { return env_int("ECSR_B200_FFD", 1) != 0; }
 bool pack_mixed() { return env_int("ECSR_B200_MIXED", 1) != 0; }
+bool force_full() { return env_int("ECSR_B200_FULL", 0) != 0; }
 #else
+constexpr bool force_full() { return false; }
 constexpr bool coop_launch() { return false; }
 constexpr bool group_force_cps1() { return false; }
 constexpr bool pack_ffd() { return true; }
@@ -1085,7 +1087,7 @@ int ecsr_b200_pack(const ecsr_host_set* sets, int32_t nsets, int64_t num_rows, i
                           &d->tile_feat, &max_tile);
         // the lean kernel covers v = 4 runs with the default blocks-per-record (or half
         // of it for g = 2, down to a quarter for g = 1) and g <= 8, and v = 1 runs of g = 1 (the reference's short set)
-        d->lean = true;  // every record's (g, v, P) has a lean-kernel variant
+        d->lean = !force_full();  // every record's (g, v, P) has a lean-kernel variant
         for (int64_t t = 0; t + 1 < static_cast<int64_t>(tstart.size()) && d->lean; ++t) {
             const uint8_t* th = arena.data() + 16ull * tstart[t];
             uint32_t nrec;
