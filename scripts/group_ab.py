@@ -37,7 +37,7 @@ def graph(body, n):
 
 
 for rep in range(2):
-    gc = graph(lambda: wl.step(stream), 5)
+    gc = graph(lambda: wl.step_chained(stream), 5)
     gg = graph(lambda: grp.spmv(xs, ys, stream=stream), 5)
     mc, _ = bench.time_graph(gc, 20, 3, stream)
     mg, _ = bench.time_graph(gg, 20, 3, stream)
