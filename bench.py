@@ -667,9 +667,60 @@ def bench_extra(name, dev, stream, args, peak):
         out.update({"value": round(gbs, 1), "unit": "GB/s", "latency_us": round(ms * 1e3, 2),
                     "latency_us_p10_p50_p90": [round(ts[int(q * (len(ts) - 1))] * 1e3, 2) for q in (0.1, 0.5, 0.9)],
                     "frac": round(gbs / peak, 4), "cold_l2": True})
+        if len(wl.launches) == 1 and len(wl.launches[0][1]) == 1:
+            out["chained"] = chained_latency(wl, stream, args, peak)
     del wl
     torch.cuda.synchronize()
     return out
+
+
+def chained_latency(wl, stream, args, peak, n_mats=8):
+    """The single SpMV's steady-state latency inside a stream of launches: n_mats
+    matrices of the same shape and sparsity (the workload's and n_mats - 1 more seeds,
+    together > the 126 MB L2, so every launch streams from HBM), launched back to back
+    round-robin (PDL-chained, graphs of 5 rounds); each extra matrix is checked against
+    the oracle first. The isolated figure above also pays the launch latency."""
+    import torch
+
+    import oracle
+    from paper_2507_12205_b200 import to_device
+    from paper_2507_12205_b200.device import spmv
+    from paper_2507_12205_b200.encoder import convert_csr
+    from paper_2507_12205_b200.generators import make_matrix
+
+    ln, (mname,) = wl.launches[0]
+    _, kind, rows, cols, sp, seed = next(m for m in WORKLOADS[wl.name]["matrices"] if m[0] == mname)
+    x, y = wl.xs[ln], wl.ys[ln]
+    x32 = x.cpu().numpy().astype(np.float32)
+    Ws, mbytes = [wl.handles[ln]], [wl.mbytes[mname]]
+    for i in range(1, n_mats):
+        ec = convert_csr(make_matrix(kind, rows, cols, sp, seed + 1000 * i, dtype=np.float32))
+        W = to_device(ec)
+        spmv(W, x, y=y, stream=stream)
+        torch.cuda.synchronize()
+        ref = oracle.spmv_ec_oracle(ec.astype(np.float16).astype(np.float32), x32, np.float32)
+        err = float(np.max(np.abs(y.cpu().numpy().astype(np.float64) - ref))) / max(float(np.max(np.abs(ref))), 1e-30)
+        if not err <= 1e-5:
+            raise SystemExit(f"parity guard failed on {wl.name} seed {seed + 1000 * i}: rel-inf {err}")
+        Ws.append(W)
+        mbytes.append(model_bytes(ec))
+    rounds = 5
+    with torch.cuda.stream(stream):
+        for W in Ws:
+            spmv(W, x, y=y, stream=stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(rounds):
+            for W in Ws:
+                spmv(W, x, y=y, stream=stream)
+    ms, _ = time_graph(g, max(4, args.steps // rounds), 3, stream)
+    per = ms / (rounds * len(Ws))
+    gbs = sum(mbytes) / len(mbytes) / (per * 1e-3) / 1e9
+    del g, Ws
+    return {"latency_us": round(per * 1e3, 2), "value": round(gbs, 1), "unit": "GB/s",
+            "frac": round(gbs / peak, 4), "matrices": n_mats, "bytes_all_matrices": int(sum(mbytes)),
+            "note": "per SpMV, launched back to back over matrices of this shape (> L2 together)"}
 
 
 def _cpu_spmv_once(m, reps):
