@@ -294,11 +294,16 @@ def host_io(pairs, stream=None, after_predecessor: bool = False) -> None:
         if nb != dst.numel() * dst.element_size():
             raise ValueError(f"host_io: src has {nb} bytes, dst {dst.numel() * dst.element_size()}")
         spans.append(_IoSpan(src.data_ptr(), dst.data_ptr(), nb))
-    dev = next((t.device for p in pairs for t in p if t.is_cuda), None)
+    devs = {t.device.index for p in pairs for t in p if t.is_cuda}
+    if len(devs) > 1:
+        raise ValueError(f"host_io: tensors on several devices {sorted(devs)}")
+    dev = torch.device("cuda", devs.pop()) if devs else (stream.device if stream is not None
+                                                         else torch.device("cuda", torch.cuda.current_device()))
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     arr = (_IoSpan * max(1, len(spans)))(*spans)
-    _lib.check(_lib.lib().ecsr_b200_host_io(arr, len(spans), _lib.IO_AFTER_PREDECESSOR if after_predecessor else 0,
-                                            ctypes.c_void_p(s.cuda_stream)), "ecsr_b200_host_io")
+    with torch.cuda.device(dev):  # the C-ABI checks device pointers against the current device
+        _lib.check(_lib.lib().ecsr_b200_host_io(arr, len(spans), _lib.IO_AFTER_PREDECESSOR if after_predecessor
+                                                else 0, ctypes.c_void_p(s.cuda_stream)), "ecsr_b200_host_io")
 
 
 def spmv_host(W: DeviceMatrix, x: np.ndarray, ordered: bool = False) -> np.ndarray:
