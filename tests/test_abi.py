@@ -118,3 +118,22 @@ def test_pack_validation_errors_need_no_gpu(corrupt, code):
     assert rc == code, _lib.last_error()
     assert not out.value
     assert _lib.last_error()
+
+
+def test_host_io_rejects_bad_calls_before_any_device_work():
+    """ecsr_b200_host_io's argument checks run on the host (no GPU needed)."""
+    from paper_2507_12205_b200.device import _IoSpan
+
+    lib = _lib.lib()
+    buf = np.zeros(64, np.float32)
+    one = (_IoSpan * 1)(_IoSpan(buf.ctypes.data, buf.ctypes.data, 256))
+    assert lib.ecsr_b200_host_io(one, 17, 0, None) == _lib.ERR_VALUE
+    assert "entries" in _lib.last_error()
+    assert lib.ecsr_b200_host_io(one, 1, 2, None) == _lib.ERR_VALUE
+    assert "flags" in _lib.last_error()
+    odd = (_IoSpan * 1)(_IoSpan(buf.ctypes.data + 4, buf.ctypes.data, 16))
+    assert lib.ecsr_b200_host_io(odd, 1, 0, None) == _lib.ERR_VALUE
+    assert "16-B aligned" in _lib.last_error()
+    # pageable host memory is not reachable by the kernel (no GPU here: also not device memory)
+    assert lib.ecsr_b200_host_io(one, 1, 0, None) == _lib.ERR_VALUE
+    assert "pinned" in _lib.last_error()
