@@ -2,7 +2,8 @@
 // (SURVEY.md §8(e), §8(f) #4): push-with-signal, PDL-chained after the shard SpMV.
 //
 // Every rank owns one device buffer (CUDA IPC, mapped by every peer):
-//   [ y_full (all ranks' rows, final layout) | pad | flags: world x 128 B | local words ]
+//   [ y_full (all ranks' rows, final layout) | pad | arrival flags: world x 128 B |
+//     ready flags: world x 128 B | local words: step, done ]
 // One exchange = ONE kernel launched right behind the rank's SpMV launch (PDL: its CTAs
 // are resident while the SpMV drains and start copying the moment it completes):
 //   CTAs (q, part) copy a slice of this rank's segments of y (its shard rows of every
@@ -17,8 +18,12 @@
 // It replaces the NCCL all-gather + index assembly of the sharded step (one exchange
 // per step, whatever the number of matrices). Steps are counted on the device (the last
 // CTA of an exchange advances the rank's step word), so graph replays stay in sync.
-// A rank's push of step s+1 can land while a slower peer still reads step s: in a
-// decode loop the next step's inputs depend on every rank's y, which orders them.
+// No push overwrites a y_full its owner still reads: before pushing step s into rank q,
+// a CTA waits for q's `ready` word (in its own buffer) to reach s; rank q sets it when
+// its own exchange s passes griddepcontrol.wait, i.e. once everything stream-ordered
+// before that exchange on q -- every reader of q's y_full of step s-1 -- has completed.
+// A y_full therefore stays valid until its owner's next exchange call, however far
+// another rank runs ahead (tests/test_gpu_exchange.py: a lagging peer).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -57,6 +62,26 @@ __global__ void __launch_bounds__(256) ecsr_xchg_kernel(const __grid_constant__ 
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(step) : "l"(p.step_word) : "memory");
     ++step;
     uint8_t* dst = p.peer_base[q];
+#ifndef ECSR_XCHG_NO_READY  // (experiment builds only: shows the race the handshake closes)
+    if (threadIdx.x == 0) {
+        // Past griddepcontrol.wait everything before this exchange on our stream has
+        // completed, the readers of our y_full's previous step included: tell rank q
+        // (ready[rank] in q's buffer) that it may push this step into us. Then wait for
+        // q to say the same before pushing into its y_full.
+        if (part == 0) {
+            unsigned long long* ready = reinterpret_cast<unsigned long long*>(
+                dst + p.flags_off + static_cast<int64_t>(p.world + p.rank) * kLine);
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ready), "l"(step) : "memory");
+        }
+        const unsigned long long* qready = reinterpret_cast<const unsigned long long*>(
+            p.peer_base[p.rank] + p.flags_off + static_cast<int64_t>(p.world + q) * kLine);
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(qready) : "memory");
+        } while (v < step);
+    }
+    __syncthreads();
+#endif
     const int64_t stride = static_cast<int64_t>(p.parts) * blockDim.x;
     for (int s = 0; s < p.nsegs; ++s) {
         const ecsr_xchg_seg sg = p.segs[s];
@@ -143,7 +168,7 @@ int ecsr_b200_xchg_create(int64_t y_bytes, int32_t rank, int32_t world, ecsr_xch
     x->world = world;
     x->y_bytes = y_bytes;
     x->flags_off = (y_bytes + kLine - 1) / kLine * kLine;
-    x->bytes = x->flags_off + static_cast<int64_t>(world + 2) * kLine;  // flags, step, done
+    x->bytes = x->flags_off + static_cast<int64_t>(2 * world + 2) * kLine;  // arrival, ready, step, done
     cudaError_t e = cudaMalloc(&x->buf, x->bytes);
     if (e == cudaSuccess) e = cudaMemset(x->buf, 0, x->bytes);
     if (e != cudaSuccess) {
@@ -209,8 +234,8 @@ int ecsr_b200_xchg_run(const ecsr_xchg* x, const void* src, void* stream) {
     p.parts = std::max(1, 32 / x->world);  // >= 32 CTAs push, each destination gets 32/world
     for (int r = 0; r < x->world; ++r) p.peer_base[r] = x->peer[r];
     p.flags_off = x->flags_off;
-    p.step_word = reinterpret_cast<unsigned long long*>(x->buf + x->flags_off + static_cast<int64_t>(x->world) * kLine);
-    p.done_word = reinterpret_cast<unsigned int*>(x->buf + x->flags_off + static_cast<int64_t>(x->world + 1) * kLine);
+    p.step_word = reinterpret_cast<unsigned long long*>(x->buf + x->flags_off + static_cast<int64_t>(2 * x->world) * kLine);
+    p.done_word = reinterpret_cast<unsigned int*>(x->buf + x->flags_off + static_cast<int64_t>(2 * x->world + 1) * kLine);
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != x->device) cudaSetDevice(x->device);

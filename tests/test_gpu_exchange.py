@@ -5,7 +5,9 @@
 * world 2 as two processes sharing the one GPU of the pool (CUDA IPC between processes
   works on one device as across NVLink): each rank runs its shards of two matrix sets in
   one grouped launch, then the exchange; after every step (eager and CUDA-graph
-  replays) both ranks' y_full must equal the oracle of every shard, concatenated.
+  replays) both ranks' y_full must equal the oracle of every shard, concatenated;
+* a lagging peer: rank 1 reads each step's y_full ~20 ms late while rank 0 runs ahead;
+  no push of a later step may land in it first (the exchange's ready handshake).
 """
 
 import os
@@ -147,3 +149,56 @@ def test_exchange_two_processes_one_gpu():
     res = dict(q.get() for _ in range(2))
     for r in range(2):
         assert len(res[r]) == 6 and max(res[r]) <= 1e-5, res
+
+
+def _lag_worker(rank, world, port, q, steps, n):
+    """Rank 1 holds every step's y_full for ~20 ms (a device sleep) before reading it,
+    while rank 0 races ahead with the next steps' pushes."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_12205_b200.exchange import PeerExchange
+
+        torch.cuda.set_device(0)
+        ex = PeerExchange(world * n, rank, world)
+        ex.plan([(0, rank * n, n)])
+        src = torch.empty(n, device="cuda")
+        snaps = [torch.empty(world * n).pin_memory() for _ in range(steps)]
+        stream = torch.cuda.Stream()
+        dist.barrier()
+        with torch.cuda.stream(stream):
+            for s in range(steps):
+                src.fill_(float(1000 * rank + s))
+                ex.run(src, stream)
+                if rank == 1:
+                    torch.cuda._sleep(40_000_000)  # ~20 ms at ~2 GHz, on the stream
+                snaps[s].copy_(ex.y, non_blocking=True)
+        stream.synchronize()
+        bad = []
+        for s in range(steps):
+            want = np.concatenate([np.full(n, 1000 * r + s, np.float32) for r in range(world)])
+            if not np.array_equal(snaps[s].numpy(), want):
+                bad.append(s)
+        q.put((rank, bad))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_lagging_peer_keeps_its_y_full():
+    """A push of step s+1 never lands in a y_full its owner still reads (step s)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lag_worker, args=(r, 2, port, q, 5, 4096)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    res = dict(q.get() for _ in range(2))
+    assert res == {0: [], 1: []}, res
