@@ -9,6 +9,10 @@ the sharded step in one launch, over peer stores instead of N
     ex = PeerExchange(y_full_floats, rank, world)       # torch.distributed initialised
     ex.plan(segments)                                   # [(src_off, dst_off, n)] floats
     ex.run(y_shard, stream)                             # -> ex.y (torch view of y_full)
+
+`ex.y` holds the step's rows until this rank's next `run` (stream order): a peer pushes
+its next step into it only after that call has passed its griddepcontrol.wait (the
+kernel's ready handshake), however far ahead the peer runs.
 """
 
 from __future__ import annotations
