@@ -237,9 +237,32 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
-            time.sleep(0.25)
             self.proc.terminate()
             self.proc.wait(timeout=5)
+
+    def load_until(self, run, stream, samples=2, timeout_s=10.0):
+        """Keep the GPU busy with `run` (the timed graph, untimed here) until nvidia-smi
+        has delivered `samples` more lines: the timed region lasts milliseconds, the
+        sampler ticks every 100 ms, so the samples are taken under the same load right
+        before and right after it."""
+        import torch
+
+        start, t0 = len(self.lines), time.time()
+        while self.proc is not None and len(self.lines) - start < samples and time.time() - t0 < timeout_s:
+            with torch.cuda.stream(stream):
+                for _ in range(20):
+                    run()
+            stream.synchronize()
+
+    def load_steps(self, run, stream, count):
+        """`count` calls of `run` (ranks whose steps exchange data run in lockstep, so
+        they pass the same count instead of waiting for samples)."""
+        import torch
+
+        with torch.cuda.stream(stream):
+            for _ in range(count):
+                run()
+        stream.synchronize()
 
     def summary(self):
         sm, mx, reasons = [], [], set()
@@ -256,10 +279,11 @@ class ClockSampler:
             for n, v in zip(names, parts[2:]):
                 if v.lower() == "active":
                     reasons.add(n)
+        window = "nvidia-smi -lms 100 while the timed graph replays back to back right before and after the timed region"
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": window}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window}
 
 
 def dist_env():
@@ -785,10 +809,12 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clocks, torch.cuda.stream(stream):
+        clocks.load_until(graph.replay, stream)
         e0.record(stream)
         for _ in range(args.steps // spg):
             graph.replay()
         e1.record(stream)
+        clocks.load_until(graph.replay, stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     # the same steps as one launch per matrix set (PDL-chained), for comparison
@@ -1107,7 +1133,9 @@ def run_sharded(args):
 
     run_step = capture(step)
     with ClockSampler(local_rank) as clocks:
+        clocks.load_steps(run_step, stream, 8000)  # ~0.5 s of steps on every rank
         ms = timed(run_step)
+        clocks.load_steps(run_step, stream, 8000)
 
     # end to end: every step copies its x in and the assembled y out; steps are pipelined
     # (x double-buffered; step i's y leaves while step i+1 computes, before exchange i+1
