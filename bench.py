@@ -244,7 +244,7 @@ class ClockSampler:
         """Keep the GPU busy with `run` (the timed graph, untimed here) until nvidia-smi
         has delivered `samples` more lines: the timed region lasts milliseconds, the
         sampler ticks every 100 ms, so the samples are taken under the same load right
-        before and right after it."""
+        after it."""
         import torch
 
         start, t0 = len(self.lines), time.time()
@@ -279,7 +279,8 @@ class ClockSampler:
             for n, v in zip(names, parts[2:]):
                 if v.lower() == "active":
                     reasons.add(n)
-        window = "nvidia-smi -lms 100 while the timed graph replays back to back right before and after the timed region"
+        window = ("nvidia-smi -lms 100 from the timed region on, while the timed graph keeps replaying back "
+                  "to back right after it (the region itself lasts milliseconds)")
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": window}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
@@ -809,12 +810,11 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clocks, torch.cuda.stream(stream):
-        clocks.load_until(graph.replay, stream)
         e0.record(stream)
         for _ in range(args.steps // spg):
             graph.replay()
         e1.record(stream)
-        clocks.load_until(graph.replay, stream)
+        clocks.load_until(graph.replay, stream, samples=3)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     # the same steps as one launch per matrix set (PDL-chained), for comparison
@@ -1133,9 +1133,8 @@ def run_sharded(args):
 
     run_step = capture(step)
     with ClockSampler(local_rank) as clocks:
-        clocks.load_steps(run_step, stream, 8000)  # ~0.5 s of steps on every rank
         ms = timed(run_step)
-        clocks.load_steps(run_step, stream, 8000)
+        clocks.load_steps(run_step, stream, 8000)  # ~0.5 s of the same steps on every rank
 
     # end to end: every step copies its x in and the assembled y out; steps are pipelined
     # (x double-buffered; step i's y leaves while step i+1 computes, before exchange i+1
