@@ -699,12 +699,13 @@ def bench_extra(name, dev, stream, args, peak):
     return out
 
 
-def chained_latency(wl, stream, args, peak, n_mats=8):
-    """The single SpMV's steady-state latency inside a stream of launches: n_mats
-    matrices of the same shape and sparsity (the workload's and n_mats - 1 more seeds,
-    together > the 126 MB L2, so every launch streams from HBM), launched back to back
-    round-robin (PDL-chained, graphs of 5 rounds); each extra matrix is checked against
-    the oracle first. The isolated figure above also pays the launch latency."""
+def chained_latency(wl, stream, args, peak, n_mats=11):
+    """The single SpMV's steady-state latency inside a stream of launches (SURVEY.md
+    §8(d) timing (ii)): n_mats matrices of the same shape and sparsity (the workload's
+    and n_mats - 1 more seeds, together > 2 x the 126 MB L2, so every launch streams from
+    HBM), launched back to back round-robin (PDL-chained, graphs of 5 rounds, >= 200
+    SpMVs timed); each extra matrix is checked against the oracle first. The isolated
+    figure above also pays the launch latency."""
     import torch
 
     import oracle
@@ -739,13 +740,30 @@ def chained_latency(wl, stream, args, peak, n_mats=8):
         for _ in range(rounds):
             for W in Ws:
                 spmv(W, x, y=y, stream=stream)
-    ms, _ = time_graph(g, max(4, args.steps // rounds), 3, stream)
-    per = ms / (rounds * len(Ws))
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
+    reps = max(4, -(-200 // (rounds * len(Ws))))
+    per_rep = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        b.record(stream)
+        b.synchronize()
+        per_rep.append(a.elapsed_time(b) / (rounds * len(Ws)))
+    per_rep.sort()
+    per = per_rep[int(0.5 * (len(per_rep) - 1))]
     gbs = sum(mbytes) / len(mbytes) / (per * 1e-3) / 1e9
     del g, Ws
-    return {"latency_us": round(per * 1e3, 2), "value": round(gbs, 1), "unit": "GB/s",
-            "frac": round(gbs / peak, 4), "matrices": n_mats, "bytes_all_matrices": int(sum(mbytes)),
-            "note": "per SpMV, launched back to back over matrices of this shape (> L2 together)"}
+    return {"latency_us": round(per * 1e3, 2),
+            "latency_us_p10_p50_p90": [round(per_rep[int(q * (len(per_rep) - 1))] * 1e3, 2) for q in (0.1, 0.5, 0.9)],
+            "value": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / peak, 4), "matrices": n_mats,
+            "spmvs_timed": reps * rounds * n_mats, "bytes_all_matrices": int(sum(mbytes)),
+            "note": "median per SpMV over graph replays, launched back to back over matrices of this shape "
+                    "(> 2 x L2 together)"}
 
 
 def _cpu_spmv_once(m, reps):
