@@ -436,6 +436,20 @@ def run_reference(args):
     par_s = max(t for t, _ in res) + t_sum
     par_err = max(float(np.max(np.abs(ysum[n] - y_ref[n])) / max(float(np.max(np.abs(y_ref[n]))), 1e-30))
                   for n in order)
+    # 4. context: the per-call container validation the executor runs
+    #    by default (validate=True) and the f64 CSR oracle, once per matrix of the layer
+    from ecsr import core
+
+    context = {"validate_container_ms": {}, "spmv_oracle_f64_ms": {}}
+    for n in order:
+        a = time.perf_counter()
+        executor.validate_container(ecs[n])
+        context["validate_container_ms"][n] = round((time.perf_counter() - a) * 1e3, 1)
+        csr = storage.decode_ec_csr(ecs[n])
+        a = time.perf_counter()
+        core.spmv_oracle(csr, xin[n].astype(np.float64))
+        context["spmv_oracle_f64_ms"][n] = round((time.perf_counter() - a) * 1e3, 1)
+    context["layer_ms"] = {k: round(sum(v.values()), 1) for k, v in list(context.items())}
     libs = loaded_native_libs()
     if any("libecsr_b200" in p for p in libs):
         raise SystemExit(f"reference arm loaded this repo's library: {libs}")
@@ -456,6 +470,7 @@ def run_reference(args):
                       "partial_y_summed": True, "rel_inf_vs_single_process": par_err,
                       "note": "secondary: each matrix's block sets split into groups, one process "
                               "each; step = slowest group + the partial-y sum"},
+        "context": context,
         "inputs": {"encoder": encoder, "encode_s": enc_s, "sha256_matches_pinned": hash_ok},
         "native_so_loaded": libs,
     }
