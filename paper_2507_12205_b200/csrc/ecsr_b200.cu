@@ -424,10 +424,14 @@ constexpr int64_t kRecordCap = 24 * 1024;
 // warps without work (fewer resident records than warps): a run's AVERAGE record is
 // also held to ~rec_cap() = half a tile (ECSR_B200_RECCAP overrides, for tuning).
 #ifdef ECSR_B200_TUNING
-int64_t rec_max() { return std::max(512, env_int("ECSR_B200_RECMAX", static_cast<int>(kRecordCap))); }
+int64_t rec_max() {
+    return std::max(512, env_int("ECSR_B200_RECMAX", static_cast<int>(std::min<int64_t>(kRecordCap, tile_target() - 16))));
+}
 int64_t rec_cap() { return std::max(512, env_int("ECSR_B200_RECCAP", tile_target() / 2)); }
 #else
-int64_t rec_max() { return kRecordCap; }
+// A record wider than the tile target would get a tile of its own and stretch every
+// stage of the pool to its size (fewer, emptier stages): P halves until it fits.
+int64_t rec_max() { return std::min<int64_t>(kRecordCap, tile_target() - 16); }
 int64_t rec_cap() { return tile_target() / 2; }
 #endif
 
