@@ -176,8 +176,8 @@ void* ecsr_b200_xchg_y(const ecsr_xchg* xchg);
 void ecsr_b200_xchg_free(ecsr_xchg* xchg);
 /* A step's host traffic as one PDL-chained kernel (end-to-end leg):
  * copies each span (src -> dst; device memory of the current device or pinned host
- * memory, which the GPU reaches through its UVA mapping; 16-B aligned, bytes a multiple
- * of 16) with plain loads/stores, in the stream's launch chain instead of on a copy
+ * memory, which the GPU reaches through its UVA mapping; src and dst 16-B aligned, any
+ * byte count) with plain loads/stores, in the stream's launch chain instead of on a copy
  * stream, so the next SpMV keeps its programmatic edge (csrc/ecsr_hostio.cu). Default:
  * the copies overlap the preceding launch and the kernel completes after it (the spans
  * must not be written by that launch); ECSR_IO_AFTER_PREDECESSOR: wait for it first

@@ -40,6 +40,7 @@ struct IoParams {
     const uint4* src[kMaxSpans];
     uint4* dst[kMaxSpans];
     long long end[kMaxSpans];  // inclusive prefix sum of the spans' 16-B chunks
+    int tail[kMaxSpans];       // bytes past the span's last whole 16-B chunk (0..15)
     int n;
     int wait_first;
 };
@@ -76,6 +77,13 @@ __global__ void __launch_bounds__(kThreads, 16) ecsr_host_io_kernel(const __grid
         for (int u = 0; u < kUnroll; ++u)
             if (d[u]) *d[u] = v[u];
     }
+    if (blockIdx.x == 0 && threadIdx.x < p.n && p.tail[threadIdx.x]) {  // ragged ends, byte by byte
+        const int s = threadIdx.x;
+        const long long whole = p.end[s] - (s ? p.end[s - 1] : 0);
+        const uint8_t* a = reinterpret_cast<const uint8_t*>(p.src[s] + whole);
+        uint8_t* b = reinterpret_cast<uint8_t*>(p.dst[s] + whole);
+        for (int k = 0; k < p.tail[s]; ++k) b[k] = a[k];
+    }
     if (!p.wait_first) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
@@ -106,9 +114,8 @@ int ecsr_b200_host_io(const ecsr_io_span* spans, int32_t nspans, int32_t flags, 
     long long chunks = 0;
     for (int i = 0; i < nspans; ++i) {
         const ecsr_io_span& s = spans[i];
-        if (s.bytes < 0 || (s.bytes & 15) || ((reinterpret_cast<uintptr_t>(s.src) |
-                                               reinterpret_cast<uintptr_t>(s.dst)) & 15))
-            return fail(ECSR_ERR_VALUE, "span " + std::to_string(i) + ": src, dst and bytes must be 16-B aligned");
+        if (s.bytes < 0 || ((reinterpret_cast<uintptr_t>(s.src) | reinterpret_cast<uintptr_t>(s.dst)) & 15))
+            return fail(ECSR_ERR_VALUE, "span " + std::to_string(i) + ": src and dst must be 16-B aligned");
         if (s.bytes && (!s.src || !s.dst)) return fail(ECSR_ERR_VALUE, "span " + std::to_string(i) + ": null pointer");
         if (s.bytes && (!mapped(s.src, device) || !mapped(s.dst, device)))
             return fail(ECSR_ERR_VALUE, "span " + std::to_string(i) +
@@ -118,6 +125,7 @@ int ecsr_b200_host_io(const ecsr_io_span* spans, int32_t nspans, int32_t flags, 
         p.src[p.n] = static_cast<const uint4*>(s.src);
         p.dst[p.n] = static_cast<uint4*>(s.dst);
         chunks += s.bytes / 16;
+        p.tail[p.n] = static_cast<int>(s.bytes & 15);
         p.end[p.n++] = chunks;
     }
     p.wait_first = (flags & ECSR_IO_AFTER_PREDECESSOR) ? 1 : 0;

@@ -279,7 +279,7 @@ def host_io(pairs, stream=None, after_predecessor: bool = False) -> None:
     """A step's host traffic as one kernel in the stream's launch chain
     (`ecsr_b200_host_io`, csrc/ecsr_hostio.cu): copies every (src, dst) tensor pair --
     CUDA tensors of the current device or pinned host tensors, same byte size, 16-B
-    aligned, contiguous -- without a copy stream, so the next SpMV keeps its PDL edge.
+    aligned starts, contiguous -- without a copy stream, so the next SpMV keeps its PDL edge.
     The copies overlap the preceding launch unless `after_predecessor` (then they read
     what it wrote); the caller keeps the preceding launch off the spans."""
     torch = _torch()

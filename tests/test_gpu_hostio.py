@@ -55,6 +55,24 @@ def test_many_spans_and_large_span():
     assert torch.equal(big_d.cpu(), big_h)
 
 
+def test_ragged_byte_counts():
+    """Spans need 16-B aligned starts, not 16-B multiples: odd fp16 lengths, a 3-float
+    span, a 1-byte span."""
+    pairs, outs = [], []
+    for n, dt in [(4097, torch.float16), (3, torch.float32), (1, torch.uint8), (33, torch.float16)]:
+        h = (torch.arange(n) % 251).to(dt).pin_memory()
+        d = torch.zeros(n, dtype=dt, device="cuda")
+        pairs.append((h, d))
+        outs.append((h, d))
+    back = torch.zeros(4097, dtype=torch.float16).pin_memory()
+    host_io(pairs)
+    host_io([(outs[0][1], back)], after_predecessor=True)
+    torch.cuda.synchronize()
+    for h, d in outs:
+        assert torch.equal(d.cpu(), h)
+    assert torch.equal(back, outs[0][0])
+
+
 def test_empty_call_keeps_the_chain():
     host_io([])
     host_io([], after_predecessor=True)
